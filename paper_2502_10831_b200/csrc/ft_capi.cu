@@ -1,0 +1,441 @@
+// ft_capi.cu -- the extern "C" boundary (include/fasttrig_b200.h).
+//
+// Argument validation, status codes and a thread-local error string; the
+// host-pointer batch entry points (the reference's std::span -> std::vector
+// API, R:proj/include/fasttrig/kernels.hpp:84-94) as a chunked H2D / K1 / D2H
+// pipeline over three streams; grid sizing; the once-per-process threshold
+// search that lets K1 replace two divisions and a compare chain by integer-
+// ordered compares.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "ft_internal.h"
+
+namespace ft {
+namespace {
+
+thread_local std::string g_err;
+std::atomic<std::uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return FT_OK;
+  (void)cudaGetLastError();  // clear sticky-free errors
+  const int code = e == cudaErrorMemoryAllocation ? FT_ERR_OOM
+                   : e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ? FT_ERR_NO_DEVICE
+                                                                                 : FT_ERR_CUDA;
+  return fail(code, std::string(where) + ": " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e));
+}
+
+// ---- thresholds (host, binary64, no contraction: see Makefile flags) ----
+template <class Pred>
+double first_true(double lo, double hi, Pred pred) {
+  // pred is monotone false..true on [lo, hi], lo >= 0, pred(lo) false,
+  // pred(hi) true.  Bisect on bit patterns (ordered like the values for >= 0).
+  std::uint64_t l, h;
+  std::memcpy(&l, &lo, 8);
+  std::memcpy(&h, &hi, 8);
+  while (h - l > 1) {
+    const std::uint64_t m = l + (h - l) / 2;
+    double dm;
+    std::memcpy(&dm, &m, 8);
+    if (pred(dm)) h = m;
+    else l = m;
+  }
+  double r;
+  std::memcpy(&r, &h, 8);
+  return r;
+}
+
+Thresholds compute_thresholds() {
+  Thresholds t{};
+  volatile double hp = kHalfPi;  // keep the divisions as IEEE divisions
+  for (int j = 1; j <= 3; ++j) {
+    t.quad[j - 1] = first_true(0.0, kTwoPi, [&](double r) { return std::floor(r / hp) >= j; });
+  }
+  t.guard = first_true(0.0, kHalfPi,
+                       [&](double red) { return std::fabs(red - hp) < kTanPoleGuard; });
+  return t;
+}
+
+const Thresholds& thresholds() {
+  static const Thresholds t = compute_thresholds();
+  return t;
+}
+
+// ---- device info ----
+std::mutex g_mu;
+std::unordered_map<const void*, int> g_occ;  // kernel -> resident blocks/SM
+int g_sms[128] = {0};
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int check_common(int dtype, unsigned mask, std::size_t n, const void* x, void* const out[3]) {
+  if (dtype != FT_F32 && dtype != FT_F64) return fail(FT_ERR_INVALID_ARG, "dtype must be FT_F32 or FT_F64");
+  if (mask == 0 || mask > 7) return fail(FT_ERR_INVALID_ARG, "mask must select 1..3 of sin/cos/tan");
+  if (n == 0) return FT_OK;
+  if (!x) return fail(FT_ERR_INVALID_ARG, "x is NULL");
+  for (int j = 0; j < 3; ++j)
+    if ((mask & (1u << j)) && !out[j]) return fail(FT_ERR_INVALID_ARG, "a selected output pointer is NULL");
+  return FT_OK;
+}
+
+EvalArgs make_args(const void* x, std::size_t n, unsigned mask, void* const out[3],
+                   std::uint8_t* seg_sc, std::uint8_t* seg_t, int steps) {
+  EvalArgs a{};
+  a.x = x;
+  for (int j = 0; j < 3; ++j) a.out[j] = (mask & (1u << j)) ? out[j] : nullptr;
+  a.seg_sc = seg_sc;
+  a.seg_t = seg_t;
+  a.n = n;
+  a.steps = steps;
+  bool ok = aligned16(x);
+  for (int j = 0; j < 3; ++j) ok = ok && (a.out[j] == nullptr || aligned16(a.out[j]));
+  // segment bytes are written one per element; any alignment works.
+  a.vec_ok = ok ? 1 : 0;
+  a.th = thresholds();
+  return a;
+}
+
+int sqrt_kind(ft_sqrt_mode m) {
+  if (m.method == FT_SQRT_EXACT) return kExact;
+  return m.newton_steps == 1 ? kFisr1 : kFisrN;
+}
+
+int check_mode(ft_sqrt_mode m) {
+  if (m.method != FT_SQRT_EXACT && m.method != FT_SQRT_FISR)
+    return fail(FT_ERR_INVALID_ARG, "sqrt mode method must be 0 (exact) or 1 (fisr)");
+  return FT_OK;
+}
+
+// ---- host pipeline state (per device) ----
+constexpr int kPipe = 3;
+struct HostPipe {
+  std::mutex mu;
+  bool init = false;
+  cudaStream_t st[kPipe]{};
+  void* buf[kPipe][4]{};  // x, sin, cos, tan
+  std::size_t cap_bytes = 0;
+};
+HostPipe g_pipe[128];
+
+int pipe_reserve(HostPipe& p, std::size_t bytes) {
+  if (!p.init) {
+    for (auto& s : p.st) {
+      cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_status(e, "cudaStreamCreate");
+    }
+    p.init = true;
+  }
+  if (bytes <= p.cap_bytes) return FT_OK;
+  for (auto& row : p.buf)
+    for (auto& b : row) {
+      if (b) cudaFree(b);
+      b = nullptr;
+    }
+  p.cap_bytes = 0;
+  for (auto& row : p.buf)
+    for (auto& b : row) {
+      cudaError_t e = cudaMalloc(&b, bytes);
+      if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(host pipeline)");
+    }
+  p.cap_bytes = bytes;
+  return FT_OK;
+}
+
+// Chunked H2D -> kernel -> D2H over kPipe streams.  `launch(args, stream)`.
+template <class Launch>
+int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* const out[3],
+                  Launch&& launch) {
+  const std::size_t es = dtype == FT_F32 ? 4 : 8;
+  const std::size_t chunk = std::size_t(1) << 23;  // elements per chunk
+  const int dev = current_device();
+  if (dev < 0 || dev >= 128) return fail(FT_ERR_CUDA, "device index out of range");
+  HostPipe& p = g_pipe[dev];
+  std::lock_guard<std::mutex> lk(p.mu);
+  int rc = pipe_reserve(p, chunk * es);
+  if (rc) return rc;
+  const char* xb = static_cast<const char*>(x);
+  std::size_t ci = 0;
+  for (std::size_t off = 0; off < n; off += chunk, ++ci) {
+    const int k = static_cast<int>(ci % kPipe);
+    const std::size_t m = std::min(chunk, n - off);
+    cudaStream_t s = p.st[k];
+    cudaError_t e = cudaMemcpyAsync(p.buf[k][0], xb + off * es, m * es, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync H2D");
+    void* dout[3] = {p.buf[k][1], p.buf[k][2], p.buf[k][3]};
+    e = launch(p.buf[k][0], m, dout, s);
+    if (e != cudaSuccess) return cuda_status(e, "kernel launch");
+    for (int j = 0; j < 3; ++j) {
+      if (!(mask & (1u << j))) continue;
+      e = cudaMemcpyAsync(static_cast<char*>(out[j]) + off * es, dout[j], m * es,
+                          cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync D2H");
+    }
+  }
+  for (auto& s : p.st) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "cudaStreamSynchronize");
+  }
+  return FT_OK;
+}
+
+// ---- L2 flush buffer (per device) ----
+struct FlushBuf {
+  std::mutex mu;
+  void* p = nullptr;
+  std::size_t bytes = 0;
+  unsigned tick = 0;
+};
+FlushBuf g_flush[128];
+
+}  // namespace
+
+unsigned persistent_blocks(const void* fn, int threads, std::size_t work_items) {
+  const int dev = current_device();
+  int occ = 0, sms = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_occ.find(fn);
+    if (it != g_occ.end()) {
+      occ = it->second;
+    } else {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0) != cudaSuccess) occ = 1;
+      g_occ[fn] = occ;
+    }
+    if (dev >= 0 && dev < 128) {
+      if (!g_sms[dev]) cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+      sms = g_sms[dev];
+    }
+  }
+  if (occ < 1) occ = 1;
+  if (sms < 1) sms = 1;
+  const std::size_t need = (work_items + threads - 1) / threads;
+  const std::size_t full = static_cast<std::size_t>(occ) * sms;
+  return static_cast<unsigned>(std::max<std::size_t>(1, std::min(need, full)));
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+}  // namespace ft
+
+using namespace ft;
+
+extern "C" {
+
+int ft_abi_version(void) { return FT_ABI_VERSION; }
+
+const char* ft_last_error_string(void) { return g_err.c_str(); }
+
+uint64_t ft_launch_count(void) { return g_launches.load(); }
+
+int ft_segment_table(double* out49) {
+  if (!out49) return fail(FT_ERR_INVALID_ARG, "out is NULL");
+  for (int k = 0; k < 6; ++k) {
+    const Coeffs& c = kTable.seg[k];
+    const double v[7] = {c.a, c.b, c.c, c.d, c.X, c.Y, c.Z};
+    for (int j = 0; j < 7; ++j) out49[k * 7 + j] = v[j];
+  }
+  for (int j = 0; j < 7; ++j) out49[42 + j] = kTable.knots[j];
+  return FT_OK;
+}
+
+int ft_taylor_coeffs(double* s9, double* c9, double* t9) {
+  if (!s9 || !c9 || !t9) return fail(FT_ERR_INVALID_ARG, "out is NULL");
+  for (int k = 0; k < 9; ++k) {
+    s9[k] = kTaylor.sin_c[k];
+    c9[k] = kTaylor.cos_c[k];
+    t9[k] = kTaylor.tan_c[k];
+  }
+  return FT_OK;
+}
+
+int ft_thresholds(double* out4) {
+  if (!out4) return fail(FT_ERR_INVALID_ARG, "out is NULL");
+  const Thresholds& t = thresholds();
+  out4[0] = t.quad[0];
+  out4[1] = t.quad[1];
+  out4[2] = t.quad[2];
+  out4[3] = t.guard;
+  return FT_OK;
+}
+
+int ft_proposed_eval_seg(ft_dtype dtype, const void* x, size_t n, unsigned mask, ft_sqrt_mode mode,
+                         void* sin_out, void* cos_out, void* tan_out, uint8_t* seg_sc,
+                         uint8_t* seg_t, void* stream) {
+  void* out[3] = {sin_out, cos_out, tan_out};
+  int rc = check_common(dtype, mask, n, x, out);
+  if (rc) return rc;
+  if ((rc = check_mode(mode))) return rc;
+  if (n == 0) return FT_OK;
+  const bool seg = seg_sc || seg_t;
+  EvalArgs a = make_args(x, n, mask, out, seg_sc, seg_t, mode.newton_steps);
+  return cuda_status(launch_proposed(dtype, mask, sqrt_kind(mode), seg, a, as_stream(stream)),
+                     "ft_proposed_eval");
+}
+
+int ft_proposed_eval(ft_dtype dtype, const void* x, size_t n, unsigned mask, ft_sqrt_mode mode,
+                     void* sin_out, void* cos_out, void* tan_out, void* stream) {
+  return ft_proposed_eval_seg(dtype, x, n, mask, mode, sin_out, cos_out, tan_out, nullptr, nullptr,
+                              stream);
+}
+
+int ft_taylor_eval(ft_dtype dtype, const void* x, size_t n, unsigned mask, int n_terms,
+                   void* sin_out, void* cos_out, void* tan_out, void* stream) {
+  void* out[3] = {sin_out, cos_out, tan_out};
+  int rc = check_common(dtype, mask, n, x, out);
+  if (rc) return rc;
+  if (n_terms < 1 || n_terms > 9) return fail(FT_ERR_INVALID_ARG, "n_terms must be in [1, 9]");
+  if (n == 0) return FT_OK;
+  EvalArgs a = make_args(x, n, mask, out, nullptr, nullptr, n_terms);
+  return cuda_status(launch_taylor(dtype, mask, n_terms, a, as_stream(stream)), "ft_taylor_eval");
+}
+
+int ft_mirror_eval(ft_dtype dtype, const void* x, size_t n, unsigned mask, int kind,
+                   ft_sqrt_mode mode, int n_terms, void* sin_out, void* cos_out, void* tan_out,
+                   uint8_t* seg_sc, uint8_t* seg_t, void* stream) {
+  void* out[3] = {sin_out, cos_out, tan_out};
+  int rc = check_common(dtype, mask, n, x, out);
+  if (rc) return rc;
+  if (kind != 0 && kind != 1) return fail(FT_ERR_INVALID_ARG, "kind must be 0 (proposed) or 1 (taylor)");
+  if (kind == 0 && (rc = check_mode(mode))) return rc;
+  if (kind == 1 && (n_terms < 1 || n_terms > 9)) return fail(FT_ERR_INVALID_ARG, "n_terms must be in [1, 9]");
+  if (n == 0) return FT_OK;
+  EvalArgs a = make_args(x, n, mask, out, seg_sc, seg_t, mode.newton_steps);
+  return cuda_status(launch_mirror(dtype, mask, kind, mode.method, n_terms, a, as_stream(stream)),
+                     "ft_mirror_eval");
+}
+
+int ft_stats_reset(ft_stats* stats_dev, void* stream) {
+  if (!stats_dev) return fail(FT_ERR_INVALID_ARG, "stats is NULL");
+  return cuda_status(cudaMemsetAsync(stats_dev, 0, sizeof(ft_stats), as_stream(stream)),
+                     "ft_stats_reset");
+}
+
+int ft_parity_reduce(ft_dtype dtype, const void* x, size_t n, unsigned mask, int kind,
+                     ft_sqrt_mode mode, int n_terms, const void* sin_out, const void* cos_out,
+                     const void* tan_out, const void* ref_sin, const void* ref_cos,
+                     const void* ref_tan, const uint8_t* seg_sc, const uint8_t* seg_t,
+                     uint64_t ulp_tol, ft_stats* stats_dev, void* stream) {
+  void* out[3] = {const_cast<void*>(sin_out), const_cast<void*>(cos_out), const_cast<void*>(tan_out)};
+  int rc = check_common(dtype, mask, n, x, out);
+  if (rc) return rc;
+  if (!stats_dev) return fail(FT_ERR_INVALID_ARG, "stats is NULL");
+  if (kind != 0 && kind != 1) return fail(FT_ERR_INVALID_ARG, "kind must be 0 or 1");
+  if (kind == 0 && (rc = check_mode(mode))) return rc;
+  if (kind == 1 && (n_terms < 1 || n_terms > 9)) return fail(FT_ERR_INVALID_ARG, "n_terms must be in [1, 9]");
+  if (n == 0) return FT_OK;
+  CheckArgs a{};
+  a.x = x;
+  a.got[0] = sin_out;
+  a.got[1] = cos_out;
+  a.got[2] = tan_out;
+  a.ref[0] = ref_sin;
+  a.ref[1] = ref_cos;
+  a.ref[2] = ref_tan;
+  a.seg_sc = seg_sc;
+  a.seg_t = seg_t;
+  a.n = n;
+  a.mask = mask;
+  a.kind = kind;
+  a.method = mode.method;
+  a.steps = mode.newton_steps;
+  a.n_terms = n_terms;
+  a.ulp_tol = ulp_tol;
+  a.stats = stats_dev;
+  return cuda_status(launch_check(dtype, a, as_stream(stream)), "ft_parity_reduce");
+}
+
+int ft_gen_inputs(ft_dtype dtype, int dist, double lo, double hi, uint64_t seed, uint64_t offset,
+                  size_t n, void* x, void* stream) {
+  if (dtype != FT_F32 && dtype != FT_F64) return fail(FT_ERR_INVALID_ARG, "bad dtype");
+  if (dist != FT_DIST_UNIFORM && dist != FT_DIST_TAN_STRESS) return fail(FT_ERR_INVALID_ARG, "bad dist");
+  if (n == 0) return FT_OK;
+  if (!x) return fail(FT_ERR_INVALID_ARG, "x is NULL");
+  if (dist == FT_DIST_TAN_STRESS && !(hi >= lo)) return fail(FT_ERR_INVALID_ARG, "kmax < kmin");
+  return cuda_status(launch_gen(dtype, dist, lo, hi, seed, offset, n, x, as_stream(stream)),
+                     "ft_gen_inputs");
+}
+
+int ft_l2_flush(void* stream) {
+  const int dev = current_device();
+  if (dev < 0 || dev >= 128) return fail(FT_ERR_CUDA, "device index out of range");
+  FlushBuf& f = g_flush[dev];
+  std::lock_guard<std::mutex> lk(f.mu);
+  if (!f.p) {
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    f.bytes = std::max<std::size_t>(2 * static_cast<std::size_t>(l2), std::size_t(64) << 20);
+    cudaError_t e = cudaMalloc(&f.p, f.bytes);
+    if (e != cudaSuccess) {
+      f.p = nullptr;
+      return cuda_status(e, "cudaMalloc(l2 flush)");
+    }
+  }
+  return cuda_status(launch_fill(f.p, f.bytes, ++f.tick, as_stream(stream)), "ft_l2_flush");
+}
+
+int ft_host_alloc(void** p, size_t bytes) {
+  if (!p) return fail(FT_ERR_INVALID_ARG, "p is NULL");
+  return cuda_status(cudaHostAlloc(p, bytes, cudaHostAllocDefault), "cudaHostAlloc");
+}
+
+int ft_host_free(void* p) { return cuda_status(cudaFreeHost(p), "cudaFreeHost"); }
+
+int ft_proposed_batch_host(ft_dtype dtype, const void* x, size_t n, unsigned mask,
+                           ft_sqrt_mode mode, void* sin_out, void* cos_out, void* tan_out) {
+  void* out[3] = {sin_out, cos_out, tan_out};
+  int rc = check_common(dtype, mask, n, x, out);
+  if (rc) return rc;
+  if ((rc = check_mode(mode))) return rc;
+  if (n == 0) return FT_OK;
+  const int sq = sqrt_kind(mode);
+  return host_pipeline(dtype, x, n, mask, out,
+                       [&](const void* dx, std::size_t m, void* const dout[3], cudaStream_t s) {
+                         EvalArgs a = make_args(dx, m, mask, dout, nullptr, nullptr, mode.newton_steps);
+                         return launch_proposed(dtype, mask, sq, false, a, s);
+                       });
+}
+
+int ft_taylor_batch_host(ft_dtype dtype, const void* x, size_t n, unsigned mask, int n_terms,
+                         void* sin_out, void* cos_out, void* tan_out) {
+  void* out[3] = {sin_out, cos_out, tan_out};
+  int rc = check_common(dtype, mask, n, x, out);
+  if (rc) return rc;
+  if (n_terms < 1 || n_terms > 9) return fail(FT_ERR_INVALID_ARG, "n_terms must be in [1, 9]");
+  if (n == 0) return FT_OK;
+  return host_pipeline(dtype, x, n, mask, out,
+                       [&](const void* dx, std::size_t m, void* const dout[3], cudaStream_t s) {
+                         EvalArgs a = make_args(dx, m, mask, dout, nullptr, nullptr, n_terms);
+                         return launch_taylor(dtype, mask, n_terms, a, s);
+                       });
+}
+
+int ft_proposed_sin_batch(const double* xs, size_t n, ft_sqrt_mode mode, double* out) {
+  return ft_proposed_batch_host(FT_F64, xs, n, FT_OUT_SIN, mode, out, nullptr, nullptr);
+}
+int ft_proposed_cos_batch(const double* xs, size_t n, ft_sqrt_mode mode, double* out) {
+  return ft_proposed_batch_host(FT_F64, xs, n, FT_OUT_COS, mode, nullptr, out, nullptr);
+}
+int ft_proposed_tan_batch(const double* xs, size_t n, ft_sqrt_mode mode, double* out) {
+  return ft_proposed_batch_host(FT_F64, xs, n, FT_OUT_TAN, mode, nullptr, nullptr, out);
+}
+
+}  // extern "C"

@@ -1,0 +1,182 @@
+// ft_check.cu -- K3: parity + error reduction.
+//
+// For every element: ulp distance of each requested output against the oracle
+// (a host-oracle array copied to the device, or the device restatement
+// mirror_* recomputed on the fly), segment-choice agreement, +-inf / NaN
+// counts, an order-independent checksum of the output bit patterns, and the
+// error against CUDA's double-precision libm (abs, and rel with the paper's
+// |ref| > 1e-12 guard).  Per-thread accumulators are folded
+// with warp shuffles and committed with one atomic per statistic per warp.
+#include "ft_internal.h"
+
+namespace ft {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <typename T>
+struct Bits;
+template <>
+struct Bits<float> {
+  static __device__ std::uint64_t raw(float v) { return static_cast<std::uint32_t>(__float_as_uint(v)); }
+  static __device__ std::int64_t ordered(float v) {
+    const std::int32_t b = __float_as_int(v);
+    return b < 0 ? -static_cast<std::int64_t>(b & 0x7fffffff) : static_cast<std::int64_t>(b);
+  }
+  static constexpr std::uint64_t kNaN = 0x7fc00000u;
+};
+template <>
+struct Bits<double> {
+  static __device__ std::uint64_t raw(double v) { return d2u(v); }
+  static __device__ std::int64_t ordered(double v) {
+    const std::int64_t b = __double_as_longlong(v);
+    return b < 0 ? -(b & 0x7fffffffffffffffll) : b;
+  }
+  static constexpr std::uint64_t kNaN = kQuietNaN;
+};
+
+template <typename T>
+__device__ __forceinline__ std::uint64_t ulp_dist(T a, T b) {
+  const bool na = isnan(a), nb = isnan(b);
+  if (na || nb) return (na && nb) ? 0ull : ~0ull;
+  const std::int64_t ia = Bits<T>::ordered(a), ib = Bits<T>::ordered(b);
+  return ia >= ib ? static_cast<std::uint64_t>(ia) - static_cast<std::uint64_t>(ib)
+                  : static_cast<std::uint64_t>(ib) - static_cast<std::uint64_t>(ia);
+}
+
+__device__ __forceinline__ std::uint64_t warp_max(std::uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const std::uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ std::uint64_t warp_sum(std::uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sumd(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct Acc {
+  std::uint64_t n = 0;
+  std::uint64_t max_ulp[3] = {0, 0, 0}, over[3] = {0, 0, 0}, seg_mm[2] = {0, 0};
+  std::uint64_t inf[3] = {0, 0, 0}, nan[3] = {0, 0, 0}, nfin[3] = {0, 0, 0}, cks[3] = {0, 0, 0};
+  // non-negative doubles kept as bit patterns (ordered like the values)
+  std::uint64_t max_or[3] = {0, 0, 0}, max_abs[3] = {0, 0, 0}, max_rel[3] = {0, 0, 0};
+  double sum_abs[3] = {0, 0, 0}, sum_rel[3] = {0, 0, 0};
+};
+
+__device__ __forceinline__ std::uint64_t umax(std::uint64_t a, std::uint64_t b) { return a > b ? a : b; }
+
+template <typename T>
+__device__ __forceinline__ T load_ref(const CheckArgs& a, int j, std::size_t i, double x) {
+  if (a.ref[j]) return static_cast<const T*>(a.ref[j])[i];
+  int seg = 0;
+  double v;
+  if (a.kind == 0) v = mirror_proposed(c_table, j, x, a.method, a.steps, &seg);
+  else v = mirror_taylor(c_taylor, j, x, a.n_terms);
+  if constexpr (sizeof(T) == 4) return __double2float_rn(v);
+  else return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_check(const CheckArgs a) {
+  Acc acc;
+  const std::size_t tid = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
+  const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+  const T* __restrict__ x = static_cast<const T*>(a.x);
+  for (std::size_t i = tid; i < a.n; i += stride) {
+    const double xd = static_cast<double>(x[i]);
+    acc.n += 1;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if (!(a.mask & (1u << j))) continue;
+      const T got = static_cast<const T*>(a.got[j])[i];
+      const T want = load_ref<T>(a, j, i, xd);
+      const std::uint64_t u = ulp_dist<T>(got, want);
+      acc.max_ulp[j] = umax(acc.max_ulp[j], u);
+      acc.over[j] += u > a.ulp_tol;
+      const double g = static_cast<double>(got), w = static_cast<double>(want);
+      if (isfinite(g) && isfinite(w)) acc.max_or[j] = umax(acc.max_or[j], d2u(fabs(g - w)));
+      acc.inf[j] += isinf(g);
+      acc.nan[j] += isnan(g);
+      acc.cks[j] += isnan(got) ? Bits<T>::kNaN : Bits<T>::raw(got);
+      const double lib = j == 0 ? sin(xd) : j == 1 ? cos(xd) : tan(xd);
+      if (isfinite(g) && isfinite(lib)) {
+        const double e = fabs(g - lib);
+        const double r = fabs(lib) > 1e-12 ? e / fabs(lib) : 0.0;
+        acc.nfin[j] += 1;
+        acc.max_abs[j] = umax(acc.max_abs[j], d2u(e));
+        acc.max_rel[j] = umax(acc.max_rel[j], d2u(r));
+        acc.sum_abs[j] += e;
+        acc.sum_rel[j] += r;
+      }
+    }
+    if (a.kind == 0 && (a.seg_sc || a.seg_t)) {
+      int s0 = 0, s1 = 0;
+      if (a.seg_sc) {
+        (void)mirror_proposed(c_table, 0, xd, a.method, a.steps, &s0);
+        acc.seg_mm[0] += a.seg_sc[i] != static_cast<std::uint8_t>(s0);
+      }
+      if (a.seg_t) {
+        (void)mirror_proposed(c_table, 2, xd, a.method, a.steps, &s1);
+        acc.seg_mm[1] += a.seg_t[i] != static_cast<std::uint8_t>(s1);
+      }
+    }
+  }
+  // warp fold, one atomic per statistic per warp
+  ft_stats* st = a.stats;
+  const bool lead = (threadIdx.x & 31) == 0;
+  std::uint64_t v = warp_sum(acc.n);
+  if (lead && v) atomicAdd(reinterpret_cast<unsigned long long*>(&st->n_checked), v);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+#define FT_MAX(field, src)                                                              \
+  v = warp_max(src);                                                                    \
+  if (lead && v) atomicMax(reinterpret_cast<unsigned long long*>(&st->field), v);
+#define FT_SUM(field, src)                                                              \
+  v = warp_sum(src);                                                                    \
+  if (lead && v) atomicAdd(reinterpret_cast<unsigned long long*>(&st->field), v);
+    FT_MAX(max_ulp[j], acc.max_ulp[j])
+    FT_SUM(n_over_tol[j], acc.over[j])
+    FT_SUM(n_inf[j], acc.inf[j])
+    FT_SUM(n_nan[j], acc.nan[j])
+    FT_SUM(n_finite_libm[j], acc.nfin[j])
+    FT_SUM(checksum[j], acc.cks[j])
+    FT_MAX(max_abs_vs_oracle[j], acc.max_or[j])
+    FT_MAX(max_abs_vs_libm[j], acc.max_abs[j])
+    FT_MAX(max_rel_vs_libm[j], acc.max_rel[j])
+    double d = warp_sumd(acc.sum_abs[j]);
+    if (lead && d != 0.0) atomicAdd(&st->sum_abs_vs_libm[j], d);
+    d = warp_sumd(acc.sum_rel[j]);
+    if (lead && d != 0.0) atomicAdd(&st->sum_rel_vs_libm[j], d);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    FT_SUM(seg_mismatch[j], acc.seg_mm[j])
+  }
+#undef FT_MAX
+#undef FT_SUM
+}
+
+template <typename T>
+cudaError_t check_go(const CheckArgs& a, cudaStream_t s) {
+  const unsigned blocks = persistent_blocks(reinterpret_cast<const void*>(k_check<T>), kThreads, a.n);
+  k_check<T><<<blocks, kThreads, 0, s>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_check(ft_dtype dt, const CheckArgs& a, cudaStream_t s) {
+  return dt == FT_F32 ? check_go<float>(a, s) : check_go<double>(a, s);
+}
+
+}  // namespace ft

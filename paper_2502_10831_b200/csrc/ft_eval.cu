@@ -1,0 +1,247 @@
+// ft_eval.cu -- K1 (fused proposed sin/cos/tan), K2 (Taylor) and the device
+// restatement kernel, all streaming elementwise maps over HBM.
+//
+// Layout: x is one contiguous array (f32 or f64); each requested output is its
+// own contiguous array of the same dtype (three separate arrays, as the
+// reference returns three vectors from proposed_*_batch, kernels.hpp:84-94).
+// Each thread moves 16 B per access (float4 / double2) with streaming cache
+// hints; the grid is persistent (#SM x resident blocks) and grid-strides.
+#include "ft_internal.h"
+
+namespace ft {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  using type = float4;
+  static constexpr int N = 4;
+  __device__ static void unpack(const float4& v, float* o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+  __device__ static float4 pack(const float* o) { return make_float4(o[0], o[1], o[2], o[3]); }
+};
+template <>
+struct Vec<double> {
+  using type = double2;
+  static constexpr int N = 2;
+  __device__ static void unpack(const double2& v, double* o) { o[0] = v.x; o[1] = v.y; }
+  __device__ static double2 pack(const double* o) { return make_double2(o[0], o[1]); }
+};
+
+template <typename T>
+__device__ __forceinline__ T to_out(double v);
+template <>
+__device__ __forceinline__ float to_out<float>(double v) { return __double2float_rn(v); }
+template <>
+__device__ __forceinline__ double to_out<double>(double v) { return v; }
+
+// The streaming map shared by every evaluation kernel.  `op(double) -> Out3`.
+template <typename T, unsigned MASK, bool SEG, class Op>
+__device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
+  using V = Vec<T>;
+  using VT = typename V::type;
+  constexpr int VN = V::N;
+  const std::size_t tid = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
+  const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+  const T* __restrict__ x = static_cast<const T*>(a.x);
+  T* __restrict__ o0 = static_cast<T*>(a.out[0]);
+  T* __restrict__ o1 = static_cast<T*>(a.out[1]);
+  T* __restrict__ o2 = static_cast<T*>(a.out[2]);
+  std::size_t done = 0;
+  if (a.vec_ok) {
+    const std::size_t nv = a.n / VN;
+    for (std::size_t v = tid; v < nv; v += stride) {
+      T xs[VN], rs[VN], rc[VN], rt[VN];
+      std::uint8_t g0[VN], g1[VN];
+      V::unpack(__ldcs(reinterpret_cast<const VT*>(x) + v), xs);
+#pragma unroll
+      for (int j = 0; j < VN; ++j) {
+        const Out3 o = op(static_cast<double>(xs[j]));
+        rs[j] = to_out<T>(o.s);
+        rc[j] = to_out<T>(o.c);
+        rt[j] = to_out<T>(o.t);
+        g0[j] = static_cast<std::uint8_t>(o.seg_sc);
+        g1[j] = static_cast<std::uint8_t>(o.seg_t);
+      }
+      if constexpr ((MASK & kSin) != 0) __stcs(reinterpret_cast<VT*>(o0) + v, V::pack(rs));
+      if constexpr ((MASK & kCos) != 0) __stcs(reinterpret_cast<VT*>(o1) + v, V::pack(rc));
+      if constexpr ((MASK & kTan) != 0) __stcs(reinterpret_cast<VT*>(o2) + v, V::pack(rt));
+      if constexpr (SEG) {
+#pragma unroll
+        for (int j = 0; j < VN; ++j) {
+          if (a.seg_sc) a.seg_sc[v * VN + j] = g0[j];
+          if (a.seg_t) a.seg_t[v * VN + j] = g1[j];
+        }
+      }
+    }
+    done = nv * VN;
+  }
+  for (std::size_t i = done + tid; i < a.n; i += stride) {
+    const Out3 o = op(static_cast<double>(x[i]));
+    if constexpr ((MASK & kSin) != 0) o0[i] = to_out<T>(o.s);
+    if constexpr ((MASK & kCos) != 0) o1[i] = to_out<T>(o.c);
+    if constexpr ((MASK & kTan) != 0) o2[i] = to_out<T>(o.t);
+    if constexpr (SEG) {
+      if (a.seg_sc) a.seg_sc[i] = static_cast<std::uint8_t>(o.seg_sc);
+      if (a.seg_t) a.seg_t[i] = static_cast<std::uint8_t>(o.seg_t);
+    }
+  }
+}
+
+template <int SQ, unsigned MASK>
+struct ProposedOp {
+  const SmemTable* tb;
+  Thresholds th;
+  int steps;
+  __device__ __forceinline__ Out3 operator()(double x) const {
+    return fast_proposed<SQ, MASK>(x, *tb, th, steps);
+  }
+};
+
+template <int NT, unsigned MASK>
+struct TaylorOp {
+  Thresholds th;
+  int n;
+  __device__ __forceinline__ Out3 operator()(double x) const { return fast_taylor<NT, MASK>(x, th, n); }
+};
+
+// Device restatement: each function evaluated separately, exactly as the
+// reference scalar code does (kernels.hpp:46-67 / SPEC.md:224-247).
+template <unsigned MASK>
+struct MirrorOp {
+  int kind, method, steps, n;
+  __device__ __forceinline__ Out3 operator()(double x) const {
+    Out3 o{0.0, 0.0, 0.0, 0, 0};
+    int seg = 0;
+    if (kind == 0) {
+      if (MASK & kSin) o.s = mirror_proposed(c_table, 0, x, method, steps, &seg);
+      if (MASK & kCos) o.c = mirror_proposed(c_table, 1, x, method, steps, &seg);
+      (void)mirror_proposed(c_table, 0, x, method, steps, &o.seg_sc);
+      o.t = mirror_proposed(c_table, 2, x, method, steps, &o.seg_t);
+      if (!(MASK & kTan)) o.t = 0.0;
+    } else {
+      if (MASK & kSin) o.s = mirror_taylor(c_taylor, 0, x, n);
+      if (MASK & kCos) o.c = mirror_taylor(c_taylor, 1, x, n);
+      if (MASK & kTan) o.t = mirror_taylor(c_taylor, 2, x, n);
+    }
+    return o;
+  }
+};
+
+// ---------------- K1 ----------------
+template <typename T, int SQ, unsigned MASK, bool SEG>
+__global__ void __launch_bounds__(kThreads) k_proposed(const EvalArgs a) {
+  __shared__ SmemTable tb;
+  stage_table(&tb);
+  __syncthreads();
+  stream_map<T, MASK, SEG>(a, ProposedOp<SQ, MASK>{&tb, a.th, a.steps});
+}
+
+// ---------------- K2 ----------------
+template <typename T, int NT, unsigned MASK>
+__global__ void __launch_bounds__(kThreads) k_taylor(const EvalArgs a) {
+  stream_map<T, MASK, false>(a, TaylorOp<NT, MASK>{a.th, a.steps});
+}
+
+// ---------------- device restatement ----------------
+template <typename T, unsigned MASK>
+__global__ void __launch_bounds__(kThreads) k_mirror(const EvalArgs a, int kind, int method) {
+  stream_map<T, MASK, true>(a, MirrorOp<MASK>{kind, method, a.steps, a.steps});
+}
+
+template <class K>
+cudaError_t go(K kernel, const EvalArgs& a, cudaStream_t s) {
+  const unsigned blocks = persistent_blocks(reinterpret_cast<const void*>(kernel), kThreads, a.n);
+  kernel<<<blocks, kThreads, 0, s>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+#define FT_MASK_SWITCH(MASK_VAR, EXPR_OF_M)   \
+  switch (MASK_VAR) {                         \
+    case 1: { constexpr unsigned M = 1; return EXPR_OF_M; } \
+    case 2: { constexpr unsigned M = 2; return EXPR_OF_M; } \
+    case 3: { constexpr unsigned M = 3; return EXPR_OF_M; } \
+    case 4: { constexpr unsigned M = 4; return EXPR_OF_M; } \
+    case 5: { constexpr unsigned M = 5; return EXPR_OF_M; } \
+    case 6: { constexpr unsigned M = 6; return EXPR_OF_M; } \
+    case 7: { constexpr unsigned M = 7; return EXPR_OF_M; } \
+    default: return cudaErrorInvalidValue;    \
+  }
+
+template <typename T, int SQ, bool SEG>
+cudaError_t proposed_t(unsigned mask, const EvalArgs& a, cudaStream_t s) {
+  FT_MASK_SWITCH(mask, (go(k_proposed<T, SQ, M, SEG>, a, s)))
+}
+
+template <typename T, int NT>
+cudaError_t taylor_t(unsigned mask, const EvalArgs& a, cudaStream_t s) {
+  FT_MASK_SWITCH(mask, (go(k_taylor<T, NT, M>, a, s)))
+}
+
+template <typename T, unsigned M>
+cudaError_t mirror_go(const EvalArgs& a, int kind, int method, cudaStream_t s) {
+  const unsigned blocks =
+      persistent_blocks(reinterpret_cast<const void*>(k_mirror<T, M>), kThreads, a.n);
+  k_mirror<T, M><<<blocks, kThreads, 0, s>>>(a, kind, method);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t mirror_t(unsigned mask, const EvalArgs& a, int kind, int method, cudaStream_t s) {
+  FT_MASK_SWITCH(mask, (mirror_go<T, M>(a, kind, method, s)))
+}
+
+template <typename T>
+cudaError_t proposed_dt(unsigned mask, int sq, bool seg, const EvalArgs& a, cudaStream_t s) {
+  if (seg) {
+    switch (sq) {
+      case kExact: return proposed_t<T, kExact, true>(mask, a, s);
+      case kFisr1: return proposed_t<T, kFisr1, true>(mask, a, s);
+      default: return proposed_t<T, kFisrN, true>(mask, a, s);
+    }
+  }
+  switch (sq) {
+    case kExact: return proposed_t<T, kExact, false>(mask, a, s);
+    case kFisr1: return proposed_t<T, kFisr1, false>(mask, a, s);
+    default: return proposed_t<T, kFisrN, false>(mask, a, s);
+  }
+}
+
+template <typename T>
+cudaError_t taylor_dt(unsigned mask, int n_terms, const EvalArgs& a, cudaStream_t s) {
+  switch (n_terms) {
+    case 5: return taylor_t<T, 5>(mask, a, s);
+    case 7: return taylor_t<T, 7>(mask, a, s);
+    case 9: return taylor_t<T, 9>(mask, a, s);
+    default: return taylor_t<T, 0>(mask, a, s);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_proposed(ft_dtype dt, unsigned mask, int sq, bool seg, const EvalArgs& a,
+                            cudaStream_t s) {
+  return dt == FT_F32 ? proposed_dt<float>(mask, sq, seg, a, s)
+                      : proposed_dt<double>(mask, sq, seg, a, s);
+}
+
+cudaError_t launch_taylor(ft_dtype dt, unsigned mask, int n_terms, const EvalArgs& a,
+                          cudaStream_t s) {
+  EvalArgs b = a;
+  b.steps = n_terms;  // Taylor kernels read the term count from `steps`
+  return dt == FT_F32 ? taylor_dt<float>(mask, n_terms, b, s) : taylor_dt<double>(mask, n_terms, b, s);
+}
+
+cudaError_t launch_mirror(ft_dtype dt, unsigned mask, int kind, int method, int n_terms,
+                          const EvalArgs& a, cudaStream_t s) {
+  EvalArgs b = a;
+  if (kind == 1) b.steps = n_terms;
+  return dt == FT_F32 ? mirror_t<float>(mask, b, kind, method, s)
+                      : mirror_t<double>(mask, b, kind, method, s);
+}
+
+}  // namespace ft

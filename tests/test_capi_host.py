@@ -1,0 +1,104 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol
+include/fasttrig_b200.h declares, carries the reference's constants bit for
+bit, and rejects bad arguments before touching CUDA."""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from oracle import oracle as O
+
+HEADER = os.path.join(ROOT, "include", "fasttrig_b200.h")
+
+
+def declared_symbols() -> set[str]:
+    src = open(HEADER).read()
+    return set(re.findall(r"^\s*(?:int|uint64_t|const char\*)\s+(ft_\w+)\s*\(", src, re.M))
+
+
+def test_exports_every_declared_symbol(ft):
+    from paper_2502_10831_b200 import _lib
+
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    assert syms == set(_lib.EXPORTS)
+    L = _lib.lib()
+    for s in syms:
+        assert hasattr(L, s), s
+    nm = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    for s in syms:
+        assert re.search(rf"\bT {s}\b", nm), s
+    assert L.ft_abi_version() == 1
+
+
+def test_device_table_is_reference_table(ft, golden):
+    t = ft.segment_table()
+    assert np.array_equal(t.view(np.uint64), golden["segment_table"].view(np.uint64))
+
+
+def test_taylor_coefficients_match_oracle(ft):
+    s, c, t = ft.taylor_coeffs()
+    a = [np.empty(9) for _ in range(3)]
+    O.port().ora_taylor_coeffs(a[0].ctypes.data, a[1].ctypes.data, a[2].ctypes.data)
+    for x, y in zip((s, c, t), a):
+        assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
+
+
+def test_thresholds_are_exact(ft):
+    """quad[j] is the least r >= 0 with floor(r / (pi/2)) >= j+1, and guard the least
+    red with |red - pi/2| < 1e-3 (IEEE division/subtraction, as in reduction.hpp)."""
+    th = ft.thresholds()
+    hp = 0.5 * math.pi
+    for j in range(3):
+        t = th[j]
+        below = np.nextafter(t, 0.0)
+        assert math.floor(t / hp) >= j + 1 and math.floor(below / hp) < j + 1
+        assert abs(t - (j + 1) * hp) < 1e-14
+    g = th[3]
+    assert abs(g - hp) < 1e-3 and not abs(np.nextafter(g, 0.0) - hp) < 1e-3
+
+
+def test_invalid_arguments_fail_without_gpu(ft):
+    from paper_2502_10831_b200 import _lib
+
+    L = _lib.lib()
+    m = _lib.SqrtModeC(1, 1)
+    x = C.c_void_p(16)
+    assert L.ft_proposed_eval(7, x, 4, 7, m, x, x, x, None) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_proposed_eval(1, x, 4, 0, m, x, x, x, None) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_proposed_eval(1, x, 4, 8, m, x, x, x, None) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_proposed_eval(1, None, 4, 1, m, x, None, None, None) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_proposed_eval(1, x, 4, 3, m, x, None, None, None) == _lib.FT_ERR_INVALID_ARG
+    assert b"NULL" in L.ft_last_error_string()
+    assert L.ft_proposed_eval(1, x, 4, 1, _lib.SqrtModeC(5, 1), x, None, None, None) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_taylor_eval(1, x, 4, 1, 0, x, None, None, None) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_taylor_eval(1, x, 4, 1, 10, x, None, None, None) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_gen_inputs(1, 9, 0.0, 1.0, 1, 0, 4, x, None) == _lib.FT_ERR_INVALID_ARG
+    # n == 0 is a no-op success (the reference maps an empty span to an empty vector)
+    assert L.ft_proposed_eval(1, None, 0, 7, m, None, None, None, None) == 0
+    assert L.ft_proposed_sin_batch(None, 0, m, None) == 0
+
+
+def test_python_mirror_sqrtmode_semantics():
+    from paper_2502_10831_b200 import SqrtMode
+
+    assert SqrtMode() == SqrtMode(1, 1)  # fisr.hpp:17-18 default fisr(1)
+    assert SqrtMode.exact() == SqrtMode(0, 0)
+    assert SqrtMode.fisr(0) == SqrtMode(1, 1) and SqrtMode.fisr(3) == SqrtMode(1, 3)
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    """No CPU fallback: a missing .so raises instead of computing anything."""
+    from paper_2502_10831_b200 import _lib
+
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
+    with pytest.raises(_lib.FasttrigError):
+        _lib.lib()

@@ -1,0 +1,296 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle.
+
+Bar (BASELINE.json north_star): at most 2 ulp from the reference's own output
+and identical segment choice per element.  The design target -- and what these
+tests assert alongside the 2-ulp contract -- is 0 ulp: f64 outputs bitwise
+equal to proposed_*(x), f32 outputs bitwise equal to (float)proposed_*((double)x).
+"""
+from __future__ import annotations
+
+import math
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import MODES, ROOT, golden_cases, same_bits, ulp_dist
+from oracle import oracle as O
+from paper_2502_10831_b200.configs import CONFIGS, PAPER_PROTOCOL, shard
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+ULP_TOL = 2  # north_star tolerance (ulps of the output dtype)
+
+
+def dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+def check_against(x: np.ndarray, out: dict, ref: dict, fns=("sin", "cos", "tan"), seg=True):
+    for f in fns:
+        g = host(out[f])
+        d = ulp_dist(g, ref[f])
+        assert d.max() <= ULP_TOL, (f, d.max())
+        assert same_bits(g, ref[f]), f  # design target: 0 ulp
+    if seg:
+        assert np.array_equal(host(out["seg_sc"]), ref["seg_sc"])
+        assert np.array_equal(host(out["seg_t"])[: x.size], ref["seg_t"])
+
+
+def test_k1_matches_golden_reference_vectors(ft, golden):
+    n = 0
+    for case, mode, x, ref in golden_cases(golden):
+        out = ft.proposed_eval(dev(x), 7, ft.SqrtMode(*MODES[mode]), seg=True)
+        torch.cuda.synchronize()
+        check_against(x, out, ref)
+        n += x.size
+    assert n > 20000
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("mask", range(1, 8))
+def test_k1_every_mask_ragged_and_misaligned(ft, dtype, mask):
+    rng = np.random.default_rng(mask)
+    base = rng.uniform(-3e3, 3e3, 70001).astype(dtype)
+    for off in (0, 1, 3):
+        for n in (0, 1, 2, 3, 5, 17, 1023, 4097, 70001 - off):
+            x = base[off:off + n]
+            xd = dev(base)[off:off + n]  # offset views -> unaligned pointers
+            out = {nm: torch.empty(max(n + 1, 1), dtype=xd.dtype, device="cuda")[1:n + 1]
+                   for j, nm in enumerate(("sin", "cos", "tan")) if mask & (1 << j)}
+            ft.proposed_eval(xd, mask, out=out)
+            torch.cuda.synchronize()
+            if n == 0:
+                continue
+            ref = O.proposed(x, mask)
+            for f in out:
+                assert same_bits(host(out[f]), ref[f]), (off, n, f)
+
+
+@pytest.mark.parametrize("mode", list(MODES) + ["fisr3"])
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg5"])
+def test_k1_config_samples_vs_oracle(ft, cfg, mode):
+    w = CONFIGS[cfg]
+    m, s = MODES.get(mode, (1, 3))
+    n = 1 << 21
+    x = O.gen_uniform(n, w.lo, w.hi, w.seed, 12345, np.dtype(w.dtype).type)
+    out = ft.proposed_eval(dev(x), 7, ft.SqrtMode(m, s), seg=True)
+    torch.cuda.synchronize()
+    check_against(x, out, O.proposed(x, 7, m, s, seg=True))
+
+
+def test_k1_adversarial_quotients(ft):
+    """Inputs whose |x|/(2pi), |x|/pi, r/(pi/2) quotients sit within a few ulps of
+    integers: the places a non-IEEE floor(a/P) would differ (Markstein step)."""
+    rng = np.random.default_rng(3)
+    j = np.concatenate([np.arange(1, 5000), rng.integers(5000, 10**7, 200000)]).astype(np.float64)
+    base = np.concatenate([j * 2 * math.pi, j * math.pi, j * 0.5 * math.pi,
+                           rng.uniform(0, 1e15, 20000)])
+    xs = [base]
+    up, dn = base.copy(), base.copy()
+    for _ in range(4):
+        up, dn = np.nextafter(up, np.inf), np.nextafter(dn, -np.inf)
+        xs += [up, dn]
+    x = np.concatenate(xs)
+    x = np.concatenate([x, -x])
+    for m, s in ((1, 1), (0, 0)):
+        out = ft.proposed_eval(dev(x), 7, ft.SqrtMode(m, s), seg=True)
+        torch.cuda.synchronize()
+        check_against(x, out, O.proposed(x, 7, m, s, seg=True))
+        xf = x.astype(np.float32)
+        out = ft.proposed_eval(dev(xf), 7, ft.SqrtMode(m, s), seg=True)
+        torch.cuda.synchronize()
+        check_against(xf, out, O.proposed(xf, 7, m, s, seg=True))
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_device_generator_matches_host(ft, dtype):
+    for w in (CONFIGS["cfg1"], CONFIGS["cfg2"], CONFIGS["cfg5"], PAPER_PROTOCOL):
+        n = 100003
+        for off in (0, 77, (1 << 32) + 5):
+            xd = ft.gen_inputs(n, getattr(torch, dtype), 0, w.lo, w.hi, w.seed, off)
+            xh = O.gen_uniform(n, w.lo, w.hi, w.seed, off, np.dtype(dtype).type)
+            assert same_bits(host(xd), xh), (w.name, off)
+    p = PAPER_PROTOCOL
+    x = ft.gen_inputs(p.n, torch.float64, 0, p.lo, p.hi, p.seed)
+    assert host(x)[0] == -316094.96443841327
+
+
+def test_taylor_matches_oracle(ft, golden):
+    for key in sorted({k.rsplit("__", 1)[0] for k in golden if k.startswith("taylor_")}):
+        x = golden[key + "__x"]
+        nt = int(key.rsplit("__n", 1)[1])
+        out = ft.taylor_eval(dev(x), nt, 7)
+        torch.cuda.synchronize()
+        for f in ("sin", "cos", "tan"):
+            assert same_bits(host(out[f]), golden[key + "__" + f]), (key, f)
+    rng = np.random.default_rng(9)
+    for dt in (np.float32, np.float64):
+        x = rng.uniform(-2e3, 2e3, 300001).astype(dt)
+        for nt in range(1, 10):
+            for mask in (1, 2, 3, 4, 7):
+                out = ft.taylor_eval(dev(x), nt, mask)
+                torch.cuda.synchronize()
+                ref = O.taylor(x, nt, mask)
+                for f in ref:
+                    assert same_bits(host(out[f]), ref[f]), (dt, nt, mask, f)
+
+
+def test_mirror_kernel_is_the_oracle(ft):
+    """The device restatement used by K3 equals the CPU oracle bit for bit."""
+    w = CONFIGS["cfg2"]
+    x = O.gen_uniform(1 << 20, w.lo, w.hi, w.seed, 999)
+    for m, s in ((1, 1), (0, 0), (1, 2)):
+        out = ft.mirror_eval(dev(x), 7, 0, ft.SqrtMode(m, s), seg=True)
+        torch.cuda.synchronize()
+        check_against(x, out, O.proposed(x, 7, m, s, seg=True))
+    out = ft.mirror_eval(dev(x), 7, 1, n_terms=7)
+    torch.cuda.synchronize()
+    ref = O.taylor(x, 7, 7)
+    for f in ref:
+        assert same_bits(host(out[f]), ref[f])
+
+
+def test_k3_with_host_oracle_arrays(ft):
+    w = CONFIGS["cfg1"]
+    x = O.gen_uniform(1 << 20, w.lo, w.hi, w.seed, 0, np.float32)
+    xd = dev(x)
+    out = ft.proposed_eval(xd, 7, seg=True)
+    ref = O.proposed(x, 7)
+    st = ft.parity_reduce(xd, out, 7, refs={f: dev(ref[f]) for f in ref}, ulp_tol=ULP_TOL)
+    assert st["n_checked"] == x.size
+    assert st["max_ulp"] == [0, 0, 0] and st["n_over_tol"] == [0, 0, 0]
+    # checksum = wrap-around sum of the output bit patterns
+    for j, f in enumerate(("sin", "cos", "tan")):
+        assert st["checksum"][j] == int(ref[f].view(np.uint32).astype(np.uint64).sum()) % (1 << 64)
+    # an injected 1-ulp / 3-ulp error is seen
+    bad = out["sin"].clone()
+    bad[5] = torch.from_numpy(np.nextafter(ref["sin"][5:6], np.float32(np.inf))).cuda()[0]
+    bad[9] = torch.from_numpy(ref["sin"][9:10].view(np.int32) + 3).view(torch.float32).cuda()[0]
+    st = ft.parity_reduce(xd, {"sin": bad}, 1, refs={"sin": dev(ref["sin"])}, ulp_tol=ULP_TOL)
+    assert st["max_ulp"][0] == 3 and st["n_over_tol"][0] == 1
+
+
+def test_k3_full_cfg2_parity_and_paper_bounds(ft):
+    """configs[1] at full size (2^28 f64): zero mismatches against the device
+    restatement, identical segments, and the paper's error bounds vs libm."""
+    w = CONFIGS["cfg2"]
+    xd = ft.gen_inputs(w.n, torch.float64, 0, w.lo, w.hi, w.seed)
+    out = ft.proposed_eval(xd, 7, seg=True)
+    st = ft.parity_reduce(xd, out, 7, ulp_tol=ULP_TOL, check_seg=True)
+    assert st["n_checked"] == w.n
+    assert st["max_ulp"] == [0, 0, 0] and st["seg_mismatch"] == [0, 0]
+    assert st["n_nan"] == [0, 0, 0]
+    # sin/cos abs max vs libm ~1.5317e-3 (0.001532); tan rel ~6.4e-3
+    assert abs(st["max_abs_vs_libm"][0] - 1.5317e-3) < 2e-6
+    assert abs(st["max_abs_vs_libm"][1] - 1.5317e-3) < 2e-6
+    assert st["max_rel_vs_libm"][2] < 6.5e-3
+    # cross-check a sample against the CPU oracle
+    idx = slice(12345678, 12345678 + (1 << 18))
+    x = host(xd[idx])
+    check_against(x, {k: v[idx] for k, v in out.items()}, O.proposed(x, 7, seg=True))
+
+
+def test_tan_stress_cfg3_full(ft):
+    """configs[2]: 2^26 f32 near the poles; device-generated x copied to the host
+    oracle; bitwise parity, +-inf count (~68%), finite max error vs libm."""
+    w = CONFIGS["cfg3"]
+    xd = ft.gen_inputs(w.n, torch.float32, 1, w.lo, w.hi, w.seed)
+    out = ft.proposed_eval(xd, 4, seg=True)
+    x = host(xd)
+    d = x.astype(np.float64)
+    k = np.round((d - 0.5 * math.pi) / math.pi)
+    assert np.all(np.abs(d - (k * math.pi + 0.5 * math.pi)) <= 0.0501)
+    ref = O.proposed(x, 4, seg=True)
+    check_against(x, out, ref, fns=("tan",))
+    st = ft.parity_reduce(xd, out, 4, ulp_tol=ULP_TOL)
+    frac_inf = st["n_inf"][2] / w.n
+    assert 0.6 < frac_inf < 0.75
+    assert st["max_ulp"][2] == 0
+
+
+def test_cfg5_sharded_equals_unsharded(ft):
+    """configs[4] host logic on one GPU: 8 contiguous shards generated in place
+    (global index as the counter) give the same checksums and maxima as one pass,
+    and the full 2^33 array (8 shards of 2^30) has zero mismatches."""
+    w = CONFIGS["cfg5"]
+    n = 1 << 28
+    xd = ft.gen_inputs(n, torch.float32, 0, w.lo, w.hi, w.seed)
+    whole = ft.parity_reduce(xd, ft.proposed_eval(xd, 7), 7, ulp_tol=ULP_TOL)
+    del xd
+    parts = []
+    for r in range(8):
+        lo, hi = shard(n, r, 8)
+        xs = ft.gen_inputs(hi - lo, torch.float32, 0, w.lo, w.hi, w.seed, lo)
+        parts.append(ft.parity_reduce(xs, ft.proposed_eval(xs, 7), 7, ulp_tol=ULP_TOL))
+    for j in range(3):
+        assert sum(p["checksum"][j] for p in parts) % (1 << 64) == whole["checksum"][j]
+        assert max(p["max_abs_vs_libm"][j] for p in parts) == whole["max_abs_vs_libm"][j]
+        assert sum(p["n_inf"][j] for p in parts) == whole["n_inf"][j]
+    # full-size cfg5 parity, shard by shard (2^30 elements each)
+    total = 0
+    for r in range(8):
+        lo, hi = shard(w.n, r, 8)
+        xs = ft.gen_inputs(hi - lo, torch.float32, 0, w.lo, w.hi, w.seed, lo)
+        st = ft.parity_reduce(xs, ft.proposed_eval(xs, 7), 7, ulp_tol=ULP_TOL)
+        assert st["max_ulp"] == [0, 0, 0], r
+        total += st["n_checked"]
+        del xs
+        torch.cuda.empty_cache()
+    assert total == w.n
+
+
+def test_host_batch_api(ft):
+    p = PAPER_PROTOCOL
+    x = O.gen_uniform(p.n, p.lo, p.hi, p.seed)
+    ref = O.proposed(x, 7)
+    assert same_bits(ft.proposed_sin_batch(x), ref["sin"])
+    assert same_bits(ft.proposed_cos_batch(x), ref["cos"])
+    assert same_bits(ft.proposed_tan_batch(x), ref["tan"])
+    assert ft.proposed_sin_batch(np.empty(0)).size == 0
+    # chunked pipeline across several chunks, f32 fused
+    w = CONFIGS["cfg1"]
+    xf = O.gen_uniform((1 << 24) + 77, w.lo, w.hi, w.seed, 0, np.float32)
+    r = ft.proposed_batch(xf, 7)
+    ref = O.proposed(xf, 7)
+    for f in ref:
+        assert same_bits(r[f], ref[f])
+    t = ft.taylor_batch(xf[:100000], 5, 3)
+    ref = O.taylor(xf[:100000], 5, 3)
+    for f in ref:
+        assert same_bits(t[f], ref[f])
+
+
+def test_paper_protocol_bounds_from_gpu(ft):
+    """PAPER.md:240 protocol through the GPU path; host glibc as the reference."""
+    p = PAPER_PROTOCOL
+    x = O.gen_uniform(p.n, p.lo, p.hi, p.seed)
+    r = ft.proposed_batch(x, 7)
+    se = np.abs(r["sin"] - np.sin(x))
+    assert abs(se.max() - 0.001532) < 5e-7
+    te = np.abs(r["tan"] - np.tan(x)) / np.abs(np.tan(x))
+    assert abs(te.max() - 0.006394) < 5e-7
+
+
+def test_cpp_dropin_program(ft, tmp_path):
+    exe = tmp_path / "test_gpu_api"
+    libdir = os.path.join(ROOT, "paper_2502_10831_b200", "lib")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "test_gpu_api.cpp"), "-L" + libdir,
+                    "-lfasttrig_b200", "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_launch_counter_counts_kernels(ft):
+    before = ft.launch_count()
+    x = ft.gen_inputs(1000, torch.float32, 0, 0.0, 1.0, 1)
+    ft.proposed_eval(x, 7)
+    ft.taylor_eval(x, 5, 3)
+    torch.cuda.synchronize()
+    assert ft.launch_count() - before == 3
