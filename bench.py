@@ -117,27 +117,37 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU baseline
-def cpu_rate(x, threads: int, target_s: float, kind_pref: str = "reference"):
+def cpu_rate(get_x, mask: int, threads: int, target_s: float, kind_pref: str = "reference"):
     """Time the reference CPU path (oracle/_ref) -- or the C port when the reference
-    was not built -- on host array x (prefix sized to ~target_s per run).
-    Returns (gelem_per_s, kind, n_sample, seconds_per_run)."""
-    import numpy as np
-
+    was not built -- on get_x(n) (a prefix of the workload's own input stream, n sized
+    to take ~target_s).  Returns (gelem_per_s, kind, n_sample, seconds, x_sample)."""
     from oracle import oracle as O
 
     kind = "reference" if (kind_pref == "reference" and O.ref_available()) else "port"
     impl = "ref" if kind == "reference" else "port"
-    probe = x[: 1 << 16]
-    O.proposed(probe, 7, threads=threads, impl=impl)  # warm
+    probe = get_x(1 << 18)
+    O.proposed(probe, mask, threads=threads, impl=impl)  # warm
     t0 = time.perf_counter()
-    O.proposed(probe, 7, threads=threads, impl=impl)
+    O.proposed(probe, mask, threads=threads, impl=impl)
     dt = max(time.perf_counter() - t0, 1e-6)
-    n = int(min(x.size, max(1 << 16, probe.size * target_s / dt)))
-    sample = np.ascontiguousarray(x[:n])
+    n = int(min(1 << 28, max(1 << 18, probe.size * target_s / dt)))
+    x = get_x(n)
     t0 = time.perf_counter()
-    O.proposed(sample, 7, threads=threads, impl=impl)
+    O.proposed(x, mask, threads=threads, impl=impl)
     dt = time.perf_counter() - t0
-    return n / dt / 1e9, kind, n, dt
+    return x.size / dt / 1e9, kind, x.size, dt, x
+
+
+def host_inputs(w):
+    """Host copy of the first n elements of workload w's input stream (uniform
+    configs are generated on the host bit-identically to K4)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    def get(n: int):
+        return O.gen_uniform(n, w.lo, w.hi, w.seed, 0, np.dtype(w.dtype).type)
+    return get
 
 
 def host_cpu_model() -> str:
@@ -166,9 +176,7 @@ def run_reference(args) -> None:
     total_steps = args.steps + args.warmup
     per_step = max(0.2, min(2.0, 120.0 / max(total_steps, 1)))
     # sample inputs: the first elements of the same seeded stream
-    x_all = O.gen_uniform(1 << 22, w.lo, w.hi, w.seed, 0, np.dtype(w.dtype).type)
-    rate, kind, n, _ = cpu_rate(x_all, threads, per_step)
-    x = x_all[:n]
+    rate, kind, n, _, x = cpu_rate(host_inputs(w), w.mask, threads, per_step)
     impl = "ref" if kind == "reference" else "port"
     for _ in range(args.warmup):
         O.proposed(x, w.mask, threads=threads, impl=impl)
@@ -336,9 +344,13 @@ def run_ours(args) -> None:
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import oracle as O
 
-        xs = x[: 1 << 22].cpu().numpy()
         threads = O.ncpu()
-        rate, kind, ns, sec = cpu_rate(xs, threads, 10.0)
+        if w.dist == 0:
+            get = host_inputs(w)
+        else:
+            xh_all = x.cpu().numpy()
+            get = lambda m: xh_all[:m]  # noqa: E731 -- device-generated stress inputs
+        rate, kind, ns, sec, _ = cpu_rate(get, w.mask, threads, 10.0)
         cpu = {"value": round(rate, 6), "unit": "Gelem/s", "cores": threads, "kind": kind,
                "sample": f"first {ns} elements of this workload ({sec:.1f} s, one run); fused "
                          f"sin+cos+tan via the scalar reference calls over {threads} threads; "

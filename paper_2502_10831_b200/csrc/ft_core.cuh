@@ -348,12 +348,13 @@ struct Out3 {
   int seg_sc, seg_t;
 };
 
-// Fused proposed sin/cos/tan of one element (kernels.hpp:46-67).
-template <int SQ, unsigned MASK>
+// Fused proposed sin/cos/tan of one element (kernels.hpp:46-67).  SEG: also
+// produce both segment choices even for functions not in MASK.
+template <int SQ, unsigned MASK, bool SEG = false>
 __device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, const Thresholds& th,
                                               int steps) {
-  constexpr bool kSC = (MASK & (kSin | kCos)) != 0;
-  constexpr bool kT = (MASK & kTan) != 0;
+  constexpr bool kSC = (MASK & (kSin | kCos)) != 0 || SEG;
+  constexpr bool kT = (MASK & kTan) != 0 || SEG;
   const FastRed fr = fast_reduce<kSC, kT>(x, th);
   Out3 o{0.0, 0.0, 0.0, 0, 0};
   if constexpr (kSC) {

@@ -90,13 +90,13 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
   }
 }
 
-template <int SQ, unsigned MASK>
+template <int SQ, unsigned MASK, bool SEG>
 struct ProposedOp {
   const SmemTable* tb;
   Thresholds th;
   int steps;
   __device__ __forceinline__ Out3 operator()(double x) const {
-    return fast_proposed<SQ, MASK>(x, *tb, th, steps);
+    return fast_proposed<SQ, MASK, SEG>(x, *tb, th, steps);
   }
 };
 
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kThreads) k_proposed(const EvalArgs a) {
   __shared__ SmemTable tb;
   stage_table(&tb);
   __syncthreads();
-  stream_map<T, MASK, SEG>(a, ProposedOp<SQ, MASK>{&tb, a.th, a.steps});
+  stream_map<T, MASK, SEG>(a, ProposedOp<SQ, MASK, SEG>{&tb, a.th, a.steps});
 }
 
 // ---------------- K2 ----------------
