@@ -157,8 +157,10 @@ int ft_host_free(void* p);
 int ft_segment_table(double* out49);
 /* Taylor coefficients sin/cos/tan, 9 each. */
 int ft_taylor_coeffs(double* sin9, double* cos9, double* tan9);
-/* Host-computed monotone thresholds: quad[3], guard. */
-int ft_thresholds(double* out4);
+/* Monotone thresholds of the fast reduction: out8[0..3] = quad[3],
+ * guard found by host bisection against IEEE division/subtraction; out8[4..7]
+ * = the same constants as compiled into the kernels (must be identical). */
+int ft_thresholds(double* out8);
 /* Number of K1/K2/K3/K4/K5 launches issued by this process so far. */
 uint64_t ft_launch_count(void);
 const char* ft_last_error_string(void);

@@ -56,6 +56,11 @@ double first_true(double lo, double hi, Pred pred) {
   return r;
 }
 
+struct Thresholds {
+  double quad[3];
+  double guard;
+};
+
 Thresholds compute_thresholds() {
   Thresholds t{};
   volatile double hp = kHalfPi;  // keep the divisions as IEEE divisions
@@ -110,7 +115,6 @@ EvalArgs make_args(const void* x, std::size_t n, unsigned mask, void* const out[
   for (int j = 0; j < 3; ++j) ok = ok && (a.out[j] == nullptr || aligned16(a.out[j]));
   // segment bytes are written one per element; any alignment works.
   a.vec_ok = ok ? 1 : 0;
-  a.th = thresholds();
   return a;
 }
 
@@ -267,13 +271,17 @@ int ft_taylor_coeffs(double* s9, double* c9, double* t9) {
   return FT_OK;
 }
 
-int ft_thresholds(double* out4) {
-  if (!out4) return fail(FT_ERR_INVALID_ARG, "out is NULL");
+int ft_thresholds(double* out8) {
+  if (!out8) return fail(FT_ERR_INVALID_ARG, "out is NULL");
   const Thresholds& t = thresholds();
-  out4[0] = t.quad[0];
-  out4[1] = t.quad[1];
-  out4[2] = t.quad[2];
-  out4[3] = t.guard;
+  out8[0] = t.quad[0];
+  out8[1] = t.quad[1];
+  out8[2] = t.quad[2];
+  out8[3] = t.guard;
+  out8[4] = kFast.quad[0];
+  out8[5] = kFast.quad[1];
+  out8[6] = kFast.quad[2];
+  out8[7] = kFast.guard;
   return FT_OK;
 }
 

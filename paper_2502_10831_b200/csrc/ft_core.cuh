@@ -24,7 +24,8 @@
 //               * the tan pole guard |red - pi/2| < 1e-3 as one threshold
 //                 compare (monotone in red on [0, pi/2]);
 //               * sign multiplications by +-1.0 as sign-bit XORs and 0.5*v as
-//                 an exponent decrement (both exact for the values they see).
+//                 an exponent decrement (both exact for the values they see);
+//               * no clamp of red and no isfinite branch (see fast_reduce).
 //             All products/sums that the reference rounds separately stay
 //             separately rounded.
 #pragma once
@@ -107,11 +108,24 @@ constexpr TaylorCoeffs make_taylor() {
 }
 constexpr TaylorCoeffs kTaylor = make_taylor();
 
-// Host-computed monotone thresholds (see ft_capi.cu: compute_thresholds).
-struct Thresholds {
+// Constants of the fast path, compiled into constant bank 3 so every compare
+// and multiply reads them as c[][] operands.  The two derived thresholds are
+// the results of the host bisection in ft_capi.cu (compute_thresholds, run
+// against IEEE division / subtraction); ft_thresholds() returns both and
+// tests/test_capi_host.py asserts they are identical.
+struct FastConsts {
   double quad[3];  // smallest r >= 0 with floor(RN(r/(pi/2))) >= 1, 2, 3
   double guard;    // smallest red in [0,pi/2] with |RN(red - pi/2)| < 1e-3
+  double knot[5];  // segment knots k*pi/12, k = 1..5 (segments.hpp:60)
+  double pi, two_pi, half_pi, inv_two_pi;
 };
+constexpr FastConsts make_fast_consts() {
+  return FastConsts{{kHalfPi, kPi, 3.0 * kHalfPi},
+                    0x1.91de2c0cf70aep+0,
+                    {kTable.knots[1], kTable.knots[2], kTable.knots[3], kTable.knots[4], kTable.knots[5]},
+                    kPi, kTwoPi, kHalfPi, kInvTwoPi};
+}
+constexpr FastConsts kFast = make_fast_consts();
 
 // Sqrt-mode selector as a template parameter of the kernels.
 enum SqrtKind : int { kExact = 0, kFisr1 = 1, kFisrN = 2 };
@@ -125,6 +139,7 @@ enum : unsigned { kSin = 1u, kCos = 2u, kTan = 4u };
 // device code needed).  Uniform-index reads only.
 static __constant__ Table c_table = make_table();
 static __constant__ TaylorCoeffs c_taylor = make_taylor();
+static __constant__ FastConsts c_fast = make_fast_consts();
 
 __device__ __forceinline__ std::uint64_t d2u(double d) {
   return static_cast<std::uint64_t>(__double_as_longlong(d));
@@ -249,38 +264,78 @@ __device__ __forceinline__ double mirror_taylor(const TaylorCoeffs& C, int which
 // ======================================================================
 // fast_*: production path (bitwise equal to mirror_* for every input)
 // ======================================================================
+//
+// Instruction budget is the design constraint (an FP64-heavy elementwise map
+// is issue-bound before it is HBM-bound on B200), so:
+//   * every constant is a kernel parameter (read as a c[0x0][] operand, never
+//     re-materialised into registers inside the loop);
+//   * compares are DSETP (one issue slot, exact) and their predicates feed
+//     SELs directly -- no integer quadrant / segment numbers are formed;
+//   * the quadrant fold is one DADD of a selected base and a sign-selected r
+//     (reference: {r, pi-r, r-pi, 2pi-r}); the reference's final clamp of red
+//     to [0, pi/2] is provably a no-op once r is in [0, 2pi)
+//     (tests/test_capi_host.py::test_fold_needs_no_clamp checks the quadrant
+//     edges), so it is not executed;
+//   * non-finite x needs no branch: the r clamp is written so NaN survives it
+//     (ordered compares are false for NaN), every later step propagates NaN,
+//     and all segment compares fail (segment 0, like the reference).
 
-// Coefficients staged in shared memory as pairs so one LDS.128 fetches two
-// (lanes that land in the same segment broadcast; six segments span 96 B, so
-// a warp's request never bank-conflicts).
+// Per-segment coefficient row in shared memory.  80-byte stride: the six rows'
+// 16-byte chunks fall in disjoint banks (80k/4 mod 32 = 0,20,8,28,16,4), so a
+// warp's LDS.128 never conflicts whichever segments its lanes pick.
+struct alignas(16) SegRow {
+  double a, b, c, d, X, Y, Z, pad0, pad1, pad2;
+};
+constexpr unsigned kRowBytes = sizeof(SegRow);
+static_assert(kRowBytes == 80, "row stride");
+
 struct SmemTable {
-  double2 ab[6];
-  double2 cd[6];
-  double2 xy[6];
-  double z[6];
+  SegRow row[6];
 };
 
 __device__ __forceinline__ void stage_table(SmemTable* s) {
   for (int i = threadIdx.x; i < 6; i += blockDim.x) {
     const Coeffs& c = c_table.seg[i];
-    s->ab[i] = make_double2(c.a, c.b);
-    s->cd[i] = make_double2(c.c, c.d);
-    s->xy[i] = make_double2(c.X, c.Y);
-    s->z[i] = c.Z;
+    s->row[i] = SegRow{c.a, c.b, c.c, c.d, c.X, c.Y, c.Z, 0.0, 0.0, 0.0};
   }
 }
 
+// Byte offset of the row for reduced angle `red` (segments.hpp:70-73: knot k
+// opens segment k).  NaN -> row 0.
+__device__ __forceinline__ unsigned seg_off(double red) {
+  const FastConsts& K = c_fast;
+  unsigned off = 0;
+  off = red >= K.knot[0] ? 1 * kRowBytes : off;
+  off = red >= K.knot[1] ? 2 * kRowBytes : off;
+  off = red >= K.knot[2] ? 3 * kRowBytes : off;
+  off = red >= K.knot[3] ? 4 * kRowBytes : off;
+  off = red >= K.knot[4] ? 5 * kRowBytes : off;
+  return off;
+}
+
+__device__ __forceinline__ const SegRow& row_at(const SmemTable& tb, unsigned off) {
+  return *reinterpret_cast<const SegRow*>(reinterpret_cast<const char*>(&tb) + off);
+}
+
+__device__ __forceinline__ double xor_hi(double v, unsigned bits) {
+  return __hiloint2double(__double2hiint(v) ^ static_cast<int>(bits), __double2loint(v));
+}
+
+// v^(-1/2) for the evaluation domain (radicand in [1.98e5, 8.9e5]; tan
+// denominator > 0.63 outside the pole window -- the only lanes whose tan value
+// is kept).  fisr.hpp:31-46 without the NaN guard, which cannot fire there;
+// 0.5*v as an exponent decrement (exact for these normal v).
 template <int SQ>
 __device__ __forceinline__ double fast_rsqrt(double v, int steps) {
-  // Domain: v is a radicand in [1.98e5, 8.9e5] or a tan denominator > 0.63
-  // for every finite x outside the pole guard (the only lanes whose value is
-  // kept), so the NaN guard of fisr.hpp:32-34 never fires and 0.5*v is an
-  // exact exponent decrement.
   if constexpr (SQ == kExact) {
     return __ddiv_rn(1.0, __dsqrt_rn(v));
   } else {
-    double y = u2d(kFisrMagic - (d2u(v) >> 1));
-    const double half_v = u2d(d2u(v) - (1ull << 52));
+    const unsigned hi = static_cast<unsigned>(__double2hiint(v));
+    const unsigned lo = static_cast<unsigned>(__double2loint(v));
+    const unsigned long long sh = (static_cast<unsigned long long>(hi >> 1) << 32) |
+                                  static_cast<unsigned long long>(__funnelshift_r(lo, hi, 1));
+    double y = u2d(kFisrMagic - sh);
+    const double half_v = __hiloint2double(static_cast<int>(hi - 0x00100000u), static_cast<int>(lo));
     if constexpr (SQ == kFisr1) {
       y = __dmul_rn(y, __dsub_rn(1.5, __dmul_rn(__dmul_rn(half_v, y), y)));
     } else {
@@ -292,55 +347,54 @@ __device__ __forceinline__ double fast_rsqrt(double v, int steps) {
 }
 
 struct FastRed {
-  double red;    // sin/cos reduced angle
-  double redt;   // tan reduced angle
-  bool neg_s, neg_c, neg_t;
-  bool guard;    // tan inside the pole window
-  bool finite;
+  double red;      // sin/cos reduced angle (reduction.hpp:59-79), NaN for non-finite x
+  double redt;     // tan reduced angle (reduction.hpp:83-93)
+  unsigned neg_s;  // sign-bit masks (0 or 0x80000000) to XOR into the results
+  unsigned neg_c;
+  unsigned neg_t;
+  bool guard;      // tan pole window (kernels.hpp:62)
 };
 
+constexpr unsigned kHiPi = 0x400921fbu, kHiTwoPi = 0x401921fbu, kHiMinusPi = 0xc00921fbu;
+constexpr unsigned kLoPi = 0x54442d18u;  // pi, -pi, 2pi share the low word
+
 template <bool NEED_SC, bool NEED_T>
-__device__ __forceinline__ FastRed fast_reduce(double x, const Thresholds& th) {
-  FastRed o;
-  o.finite = isfinite(x);
+__device__ __forceinline__ FastRed fast_reduce(double x) {
+  const FastConsts& K = c_fast;
+  FastRed o{};
   const double a = fabs(x);
-  // q1 = RN(a / 2pi) exactly (Markstein): y = RN(1/2pi), q0 faithful.
-  const double q0 = __dmul_rn(a, kInvTwoPi);
-  const double rem = __fma_rn(-q0, kTwoPi, a);
-  const double q1 = __fma_rn(rem, kInvTwoPi, q0);
-  const bool xneg = signbit(x);
+  // q1 = RN(a / 2pi) exactly: y = RN(1/2pi) is within 0.206*2^-53 relative, so
+  // q0 = RN(a*y) is within 0.912 ulp of a/2pi and one Markstein correction
+  // (exact FMA remainder) rounds to RN(a/2pi).
+  const double q0 = __dmul_rn(a, K.inv_two_pi);
+  const double rem = __fma_rn(-q0, K.two_pi, a);
+  const double q1 = __fma_rn(rem, K.inv_two_pi, q0);
+  const unsigned xs = static_cast<unsigned>(__double2hiint(x)) & 0x80000000u;
   if constexpr (NEED_SC) {
-    // reduction.hpp:26-30 with period 2pi
-    double r = __dsub_rn(a, __dmul_rn(kTwoPi, floor(q1)));
-    r = r < 0.0 ? 0.0 : r;
-    r = r < kTwoPi ? r : 0.0;
-    // reduction.hpp:44-52: q = min(floor(RN(r/(pi/2))), 3) via thresholds
-    const int q = (r >= th.quad[0]) + (r >= th.quad[1]) + (r >= th.quad[2]);
-    // red = {r, pi - r, r - pi, 2pi - r}[q] as one rounded add
-    const double base = q == 0 ? 0.0 : q == 1 ? kPi : q == 2 ? -kPi : kTwoPi;
-    const double red = __dadd_rn(base, flip_sign(r, q & 1));
-    o.red = red < 0.0 ? 0.0 : (red < kHalfPi ? red : kHalfPi);
-    o.neg_s = (q >= 2) != xneg;
-    o.neg_c = (q == 1) || (q == 2);
+    // reduction.hpp:26-30 (period 2pi); NaN passes the clamp unchanged
+    double r = __dsub_rn(a, __dmul_rn(K.two_pi, floor(q1)));
+    r = (r < 0.0 || r >= K.two_pi) ? 0.0 : r;
+    // reduction.hpp:44-52: q = floor(RN(r/(pi/2))) = p1 + p2 + p3
+    const bool p1 = r >= K.quad[0], p2 = r >= K.quad[1], p3 = r >= K.quad[2];
+    const bool odd = p1 ^ p2 ^ p3;
+    const unsigned bhi = p3 ? kHiTwoPi : (p2 ? kHiMinusPi : (p1 ? kHiPi : 0u));
+    const unsigned blo = p1 ? kLoPi : 0u;
+    o.red = __dadd_rn(__hiloint2double(static_cast<int>(bhi), static_cast<int>(blo)),
+                      xor_hi(r, odd ? 0x80000000u : 0u));
+    o.neg_s = (p2 ? 0x80000000u : 0u) ^ xs;  // q >= 2, odd symmetry (reduction.hpp:65-66)
+    o.neg_c = (p1 != p3) ? 0x80000000u : 0u; // q in {1, 2} (reduction.hpp:77)
   }
   if constexpr (NEED_T) {
-    // RN(a/pi) == 2*RN(a/2pi) exactly (2pi is an exact doubling of pi).
-    double r = __dsub_rn(a, __dmul_rn(kPi, floor(__dadd_rn(q1, q1))));
-    r = r < 0.0 ? 0.0 : r;
-    r = r < kPi ? r : 0.0;
-    const bool upper = r > kHalfPi;
-    const double red = __dadd_rn(upper ? kPi : 0.0, flip_sign(r, upper));
-    o.redt = red < 0.0 ? 0.0 : (red < kHalfPi ? red : kHalfPi);
-    o.neg_t = upper != xneg;
-    o.guard = o.redt >= th.guard;
+    // RN(a/pi) == 2*RN(a/2pi) exactly (2pi is an exact doubling of pi)
+    double r = __dsub_rn(a, __dmul_rn(K.pi, floor(__dadd_rn(q1, q1))));
+    r = (r < 0.0 || r >= K.pi) ? 0.0 : r;
+    const bool up = r > K.half_pi;  // reduction.hpp:88-89
+    o.redt = __dadd_rn(__hiloint2double(up ? static_cast<int>(kHiPi) : 0, up ? static_cast<int>(kLoPi) : 0),
+                       xor_hi(r, up ? 0x80000000u : 0u));
+    o.neg_t = (up ? 0x80000000u : 0u) ^ xs;
+    o.guard = o.redt >= K.guard;
   }
   return o;
-}
-
-__device__ __forceinline__ int fast_segment(double red) {
-  constexpr double k1 = kTable.knots[1], k2 = kTable.knots[2], k3 = kTable.knots[3],
-                   k4 = kTable.knots[4], k5 = kTable.knots[5];
-  return (red >= k1) + (red >= k2) + (red >= k3) + (red >= k4) + (red >= k5);
 }
 
 struct Out3 {
@@ -351,38 +405,30 @@ struct Out3 {
 // Fused proposed sin/cos/tan of one element (kernels.hpp:46-67).  SEG: also
 // produce both segment choices even for functions not in MASK.
 template <int SQ, unsigned MASK, bool SEG = false>
-__device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, const Thresholds& th,
-                                              int steps) {
+__device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, int steps) {
   constexpr bool kSC = (MASK & (kSin | kCos)) != 0 || SEG;
   constexpr bool kT = (MASK & kTan) != 0 || SEG;
-  const FastRed fr = fast_reduce<kSC, kT>(x, th);
+  const FastRed fr = fast_reduce<kSC, kT>(x);
   Out3 o{0.0, 0.0, 0.0, 0, 0};
   if constexpr (kSC) {
-    const int k = fast_segment(fr.red);
-    o.seg_sc = fr.finite ? k : 0;
+    const unsigned off = seg_off(fr.red);
+    if constexpr (SEG) o.seg_sc = static_cast<int>(off / kRowBytes);
+    const SegRow& s = row_at(tb, off);
     const double red = fr.red;
-    const double2 xy = tb.xy[k];
-    const double rad = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(xy.x, red), xy.y), red), tb.z[k]);
+    const double rad = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(s.X, red), s.Y), red), s.Z);
     const double rs = fast_rsqrt<SQ>(rad, steps);
-    if constexpr (MASK & kSin) {
-      const double2 ab = tb.ab[k];
-      const double v = __dmul_rn(__dadd_rn(__dmul_rn(ab.x, red), ab.y), rs);
-      o.s = fr.finite ? flip_sign(v, fr.neg_s) : u2d(kQuietNaN);
-    }
-    if constexpr (MASK & kCos) {
-      const double2 cd = tb.cd[k];
-      const double v = __dmul_rn(__dadd_rn(__dmul_rn(cd.x, red), cd.y), rs);
-      o.c = fr.finite ? flip_sign(v, fr.neg_c) : u2d(kQuietNaN);
-    }
+    if constexpr ((MASK & kSin) != 0)
+      o.s = xor_hi(__dmul_rn(__dadd_rn(__dmul_rn(s.a, red), s.b), rs), fr.neg_s);
+    if constexpr ((MASK & kCos) != 0)
+      o.c = xor_hi(__dmul_rn(__dadd_rn(__dmul_rn(s.c, red), s.d), rs), fr.neg_c);
   }
   if constexpr (kT) {
-    const int k = fast_segment(fr.redt);
-    o.seg_t = !fr.finite ? 0 : fr.guard ? 255 : k;
+    const unsigned off = seg_off(fr.redt);
+    if constexpr (SEG) o.seg_t = fr.guard ? 255 : static_cast<int>(off / kRowBytes);
+    const SegRow& s = row_at(tb, off);
     const double red = fr.redt;
-    const double2 ab = tb.ab[k];
-    const double2 cd = tb.cd[k];
-    const double poly = __dadd_rn(__dmul_rn(ab.x, red), ab.y);
-    const double den = __dadd_rn(__dmul_rn(cd.x, red), cd.y);
+    const double poly = __dadd_rn(__dmul_rn(s.a, red), s.b);
+    const double den = __dadd_rn(__dmul_rn(s.c, red), s.d);
     double v;
     if constexpr (SQ == kExact) {
       v = __ddiv_rn(poly, den);
@@ -391,7 +437,7 @@ __device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, con
       v = __dmul_rn(poly, __dmul_rn(r, r));
     }
     v = fr.guard ? __longlong_as_double(0x7ff0000000000000ll) : v;
-    o.t = fr.finite ? flip_sign(v, fr.neg_t) : u2d(kQuietNaN);
+    o.t = xor_hi(v, fr.neg_t);
   }
   return o;
 }
@@ -414,29 +460,25 @@ __device__ __forceinline__ double taylor_horner(const double* c, int n, double s
 
 // Fused Taylor sin/cos/tan of one element, n nonzero terms.
 template <int NT, unsigned MASK>
-__device__ __forceinline__ Out3 fast_taylor(double x, const Thresholds& th, int n) {
+__device__ __forceinline__ Out3 fast_taylor(double x, int n) {
   constexpr bool kSC = (MASK & (kSin | kCos)) != 0;
   constexpr bool kT = (MASK & kTan) != 0;
-  const FastRed fr = fast_reduce<kSC, kT>(x, th);
+  const FastRed fr = fast_reduce<kSC, kT>(x);
   Out3 o{0.0, 0.0, 0.0, 0, 0};
   if constexpr (kSC) {
     const double s2 = __dmul_rn(fr.red, fr.red);
-    if constexpr (MASK & kSin) {
-      const double p = taylor_horner<NT>(c_taylor.sin_c, n, s2);
-      o.s = fr.finite ? flip_sign(__dmul_rn(fr.red, p), fr.neg_s) : u2d(kQuietNaN);
-    }
-    if constexpr (MASK & kCos) {
-      const double p = taylor_horner<NT>(c_taylor.cos_c, n, s2);
-      o.c = fr.finite ? flip_sign(p, fr.neg_c) : u2d(kQuietNaN);
-    }
+    if constexpr ((MASK & kSin) != 0)
+      o.s = xor_hi(__dmul_rn(fr.red, taylor_horner<NT>(c_taylor.sin_c, n, s2)), fr.neg_s);
+    if constexpr ((MASK & kCos) != 0)
+      o.c = xor_hi(taylor_horner<NT>(c_taylor.cos_c, n, s2), fr.neg_c);
   }
   if constexpr (kT) {
     const double s2 = __dmul_rn(fr.redt, fr.redt);
-    const double p = taylor_horner<NT>(c_taylor.tan_c, n, s2);
-    o.t = fr.finite ? flip_sign(__dmul_rn(fr.redt, p), fr.neg_t) : u2d(kQuietNaN);
+    o.t = xor_hi(__dmul_rn(fr.redt, taylor_horner<NT>(c_taylor.tan_c, n, s2)), fr.neg_t);
   }
   return o;
 }
+
 
 #endif  // __CUDACC__
 

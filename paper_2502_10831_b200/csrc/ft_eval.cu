@@ -93,18 +93,16 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
 template <int SQ, unsigned MASK, bool SEG>
 struct ProposedOp {
   const SmemTable* tb;
-  Thresholds th;
   int steps;
   __device__ __forceinline__ Out3 operator()(double x) const {
-    return fast_proposed<SQ, MASK, SEG>(x, *tb, th, steps);
+    return fast_proposed<SQ, MASK, SEG>(x, *tb, steps);
   }
 };
 
 template <int NT, unsigned MASK>
 struct TaylorOp {
-  Thresholds th;
   int n;
-  __device__ __forceinline__ Out3 operator()(double x) const { return fast_taylor<NT, MASK>(x, th, n); }
+  __device__ __forceinline__ Out3 operator()(double x) const { return fast_taylor<NT, MASK>(x, n); }
 };
 
 // Device restatement: each function evaluated separately, exactly as the
@@ -136,13 +134,13 @@ __global__ void __launch_bounds__(kThreads) k_proposed(const EvalArgs a) {
   __shared__ SmemTable tb;
   stage_table(&tb);
   __syncthreads();
-  stream_map<T, MASK, SEG>(a, ProposedOp<SQ, MASK, SEG>{&tb, a.th, a.steps});
+  stream_map<T, MASK, SEG>(a, ProposedOp<SQ, MASK, SEG>{&tb, a.steps});
 }
 
 // ---------------- K2 ----------------
 template <typename T, int NT, unsigned MASK>
 __global__ void __launch_bounds__(kThreads) k_taylor(const EvalArgs a) {
-  stream_map<T, MASK, false>(a, TaylorOp<NT, MASK>{a.th, a.steps});
+  stream_map<T, MASK, false>(a, TaylorOp<NT, MASK>{a.steps});
 }
 
 // ---------------- device restatement ----------------

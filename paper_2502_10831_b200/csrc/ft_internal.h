@@ -19,7 +19,6 @@ struct EvalArgs {
   std::size_t n;
   int steps;
   int vec_ok;  // all pointers aligned for 128-bit access
-  Thresholds th;
 };
 
 struct CheckArgs {

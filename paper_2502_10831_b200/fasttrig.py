@@ -228,7 +228,8 @@ def taylor_coeffs() -> tuple[np.ndarray, np.ndarray, np.ndarray]:
 
 
 def thresholds() -> np.ndarray:
-    out = np.empty(4, np.float64)
+    """[quad1, quad2, quad3, guard] by host bisection, then the compiled-in copies."""
+    out = np.empty(8, np.float64)
     L.check(L.lib().ft_thresholds(out.ctypes.data))
     return out
 

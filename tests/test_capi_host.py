@@ -56,6 +56,8 @@ def test_thresholds_are_exact(ft):
     red with |red - pi/2| < 1e-3 (IEEE division/subtraction, as in reduction.hpp)."""
     th = ft.thresholds()
     hp = 0.5 * math.pi
+    # the constants compiled into the kernels are the bisection results, bit for bit
+    assert np.array_equal(th[:4].view(np.uint64), th[4:].view(np.uint64))
     for j in range(3):
         t = th[j]
         below = np.nextafter(t, 0.0)
@@ -102,3 +104,20 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(_lib.FasttrigError):
         _lib.lib()
+
+
+def test_fold_needs_no_clamp(ft):
+    """The fast path drops the reference's final clamp of red to [0, pi/2]
+    (reduction.hpp:32-35 called from :51 and :89).  Sound because each quadrant's
+    red = RN(base +- r) is monotone in r, so its extremes sit at the quadrant
+    edges (the bisected thresholds); check every edge in IEEE binary64."""
+    th = ft.thresholds()
+    T1, T2, T3 = th[:3]
+    pi, hp, tp = math.pi, 0.5 * math.pi, 2.0 * math.pi
+    prev = lambda v: float(np.nextafter(v, 0.0))  # noqa: E731
+    nxt = lambda v: float(np.nextafter(v, 10.0))  # noqa: E731
+    assert prev(T1) <= hp                                   # q=0: red = r < T1
+    assert 0.0 <= pi - prev(T2) and pi - T1 <= hp           # q=1: red = pi - r
+    assert 0.0 <= T2 - pi and prev(T3) - pi <= hp           # q=2: red = r - pi
+    assert 0.0 <= tp - prev(tp) and tp - T3 <= hp           # q=3: red = 2pi - r
+    assert 0.0 <= pi - prev(pi) and pi - nxt(hp) <= hp      # tan upper: red = pi - r
