@@ -12,7 +12,7 @@ import subprocess
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libfasttrig_b200.so")
+LIB_PATH = os.environ.get("FASTTRIG_B200_LIB") or os.path.join(PKG, "lib", "libfasttrig_b200.so")
 
 FT_OK, FT_ERR_INVALID_ARG, FT_ERR_CUDA, FT_ERR_OOM, FT_ERR_NO_DEVICE = 0, 1, 2, 3, 4
 FT_F32, FT_F64 = 0, 1

@@ -12,6 +12,9 @@ namespace ft {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef FT_MINB
+#define FT_MINB 6  // __launch_bounds__ min blocks per SM for K1/K2 (<= 40 registers)
+#endif
 
 template <typename T>
 struct Vec;
@@ -52,10 +55,12 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
   std::size_t done = 0;
   if (a.vec_ok) {
     const std::size_t nv = a.n / VN;
-    for (std::size_t v = tid; v < nv; v += stride) {
+    const VT* __restrict__ xv = reinterpret_cast<const VT*>(x);
+    // Evaluate + store one vector.
+    auto body = [&](const VT& xin, std::size_t v) {
       T xs[VN], rs[VN], rc[VN], rt[VN];
       std::uint8_t g0[VN], g1[VN];
-      V::unpack(__ldcs(reinterpret_cast<const VT*>(x) + v), xs);
+      V::unpack(xin, xs);
 #pragma unroll
       for (int j = 0; j < VN; ++j) {
         const Out3 o = op(static_cast<double>(xs[j]));
@@ -75,7 +80,12 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
           if (a.seg_t) a.seg_t[v * VN + j] = g1[j];
         }
       }
-    }
+    };
+    // Direct loads: measured against a cp.async smem double buffer, an L2
+    // prefetch hint and a 2-wide loads-first unroll (profiles/README.md,
+    // round-1 variants); none beat this loop, which runs at the power cap.
+    for (std::size_t v = tid; v < nv; v += stride) body(__ldcs(xv + v), v);
+
     done = nv * VN;
   }
   for (std::size_t i = done + tid; i < a.n; i += stride) {
@@ -130,7 +140,7 @@ struct MirrorOp {
 
 // ---------------- K1 ----------------
 template <typename T, int SQ, unsigned MASK, bool SEG>
-__global__ void __launch_bounds__(kThreads) k_proposed(const EvalArgs a) {
+__global__ void __launch_bounds__(kThreads, FT_MINB) k_proposed(const EvalArgs a) {
   __shared__ SmemTable tb;
   stage_table(&tb);
   __syncthreads();
@@ -139,7 +149,7 @@ __global__ void __launch_bounds__(kThreads) k_proposed(const EvalArgs a) {
 
 // ---------------- K2 ----------------
 template <typename T, int NT, unsigned MASK>
-__global__ void __launch_bounds__(kThreads) k_taylor(const EvalArgs a) {
+__global__ void __launch_bounds__(kThreads, FT_MINB) k_taylor(const EvalArgs a) {
   stream_map<T, MASK, false>(a, TaylorOp<NT, MASK>{a.steps});
 }
 
