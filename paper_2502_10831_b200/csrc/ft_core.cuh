@@ -118,12 +118,14 @@ struct FastConsts {
   double guard;    // smallest red in [0,pi/2] with |RN(red - pi/2)| < 1e-3
   double knot[5];  // segment knots k*pi/12, k = 1..5 (segments.hpp:60)
   double pi, two_pi, half_pi, inv_two_pi;
+  double twelve_over_pi;  // RN(12/pi): row guess floor(red * 12/pi)
+  double two52;           // 2^52: fma.rz(red, 12/pi, 2^52) puts floor() in the low word
 };
 constexpr FastConsts make_fast_consts() {
   return FastConsts{{kHalfPi, kPi, 3.0 * kHalfPi},
                     0x1.91de2c0cf70aep+0,
                     {kTable.knots[1], kTable.knots[2], kTable.knots[3], kTable.knots[4], kTable.knots[5]},
-                    kPi, kTwoPi, kHalfPi, kInvTwoPi};
+                    kPi, kTwoPi, kHalfPi, kInvTwoPi, 12.0 / kPi, 0x1p52};
 }
 constexpr FastConsts kFast = make_fast_consts();
 
@@ -280,28 +282,43 @@ __device__ __forceinline__ double mirror_taylor(const TaylorCoeffs& C, int which
 //     (ordered compares are false for NaN), every later step propagates NaN,
 //     and all segment compares fail (segment 0, like the reference).
 
-// Per-segment coefficient row in shared memory.  80-byte stride: the six rows'
-// 16-byte chunks fall in disjoint banks (80k/4 mod 32 = 0,20,8,28,16,4), so a
-// warp's LDS.128 never conflicts whichever segments its lanes pick.
+// Per-segment coefficient row in shared memory: the coefficients plus the
+// half-open bracket [klo, khi) of reduced angles the row is valid for.
+// 80-byte stride: the 16-byte chunks of the eight rows fall in disjoint banks
+// (80k/4 mod 32 = 0,20,8,28,16,4,24,12), so a warp's LDS.128 never conflicts
+// whichever rows its lanes pick.
 struct alignas(16) SegRow {
-  double a, b, c, d, X, Y, Z, pad0, pad1, pad2;
+  double a, b, c, d, X, Y, Z;
+  double klo, khi;
+  int seg, pad;
 };
 constexpr unsigned kRowBytes = sizeof(SegRow);
 static_assert(kRowBytes == 80, "row stride");
 
+// Rows 0..5 are segments 0..5 (segments.hpp:33-66); the row is chosen by the
+// guess g = floor(red * 12/pi) (0..6 for red in [0, pi/2], 7 for NaN) and then
+// validated against its bracket.  Row 6 repeats segment 5 (red == pi/2 guesses
+// 6); row 7 never validates.  Row 0 starts at the smallest positive double,
+// not 0: a reduced angle of exactly +0 is sent to the exact path, which is what
+// makes dropping the r clamps sound (see fast_proposed).
 struct SmemTable {
-  SegRow row[6];
+  SegRow row[8];
 };
 
 __device__ __forceinline__ void stage_table(SmemTable* s) {
-  for (int i = threadIdx.x; i < 6; i += blockDim.x) {
-    const Coeffs& c = c_table.seg[i];
-    s->row[i] = SegRow{c.a, c.b, c.c, c.d, c.X, c.Y, c.Z, 0.0, 0.0, 0.0};
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  for (int i = threadIdx.x; i < 8; i += blockDim.x) {
+    const int k = i < 6 ? i : 5;
+    const Coeffs& c = c_table.seg[k];
+    const double klo = i == 0 ? __longlong_as_double(1) : i == 7 ? inf : c_table.knots[k];
+    const double khi = i >= 5 ? inf : c_table.knots[k + 1];
+    s->row[i] = SegRow{c.a, c.b, c.c, c.d, c.X, c.Y, c.Z, klo, khi, k, 0};
   }
 }
 
 // Byte offset of the row for reduced angle `red` (segments.hpp:70-73: knot k
-// opens segment k).  NaN -> row 0.
+// opens segment k).  NaN -> row 0.  (Exact search; the fast path uses the
+// bracket-validated guess instead.)
 __device__ __forceinline__ unsigned seg_off(double red) {
   const FastConsts& K = c_fast;
   unsigned off = 0;
@@ -358,7 +375,9 @@ struct FastRed {
 constexpr unsigned kHiPi = 0x400921fbu, kHiTwoPi = 0x401921fbu, kHiMinusPi = 0xc00921fbu;
 constexpr unsigned kLoPi = 0x54442d18u;  // pi, -pi, 2pi share the low word
 
-template <bool NEED_SC, bool NEED_T>
+// CLAMP: apply the reference's r clamps (NaN-preserving form).  The proposed
+// path runs without them and validates instead (fast_proposed).
+template <bool NEED_SC, bool NEED_T, bool CLAMP>
 __device__ __forceinline__ FastRed fast_reduce(double x) {
   const FastConsts& K = c_fast;
   FastRed o{};
@@ -371,9 +390,11 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
   const double q1 = __fma_rn(rem, K.inv_two_pi, q0);
   const unsigned xs = static_cast<unsigned>(__double2hiint(x)) & 0x80000000u;
   if constexpr (NEED_SC) {
-    // reduction.hpp:26-30 (period 2pi); NaN passes the clamp unchanged
+    // reduction.hpp:26-30 (period 2pi) without its two clamps: r < 0 or
+    // r >= 2pi folds to red <= 0 (or NaN), which fails the row bracket and
+    // takes the exact path (fast_proposed).
     double r = __dsub_rn(a, __dmul_rn(K.two_pi, floor(q1)));
-    r = (r < 0.0 || r >= K.two_pi) ? 0.0 : r;
+    if constexpr (CLAMP) r = (r < 0.0 || r >= K.two_pi) ? 0.0 : r;
     // reduction.hpp:44-52: q = floor(RN(r/(pi/2))) = p1 + p2 + p3
     const bool p1 = r >= K.quad[0], p2 = r >= K.quad[1], p3 = r >= K.quad[2];
     const bool odd = p1 ^ p2 ^ p3;
@@ -387,7 +408,7 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
   if constexpr (NEED_T) {
     // RN(a/pi) == 2*RN(a/2pi) exactly (2pi is an exact doubling of pi)
     double r = __dsub_rn(a, __dmul_rn(K.pi, floor(__dadd_rn(q1, q1))));
-    r = (r < 0.0 || r >= K.pi) ? 0.0 : r;
+    if constexpr (CLAMP) r = (r < 0.0 || r >= K.pi) ? 0.0 : r;
     const bool up = r > K.half_pi;  // reduction.hpp:88-89
     o.redt = __dadd_rn(__hiloint2double(up ? static_cast<int>(kHiPi) : 0, up ? static_cast<int>(kLoPi) : 0),
                        xor_hi(r, up ? 0x80000000u : 0u));
@@ -402,18 +423,41 @@ struct Out3 {
   int seg_sc, seg_t;
 };
 
+// The exact path of fast_proposed: all three functions and both segment
+// choices by the device restatement.  Out of line so the rarely-taken branch
+// costs the hot loop neither instructions nor registers.
+static __device__ __noinline__ Out3 slow_proposed(double x, int method, int steps) {
+  Out3 o;
+  o.s = mirror_proposed(c_table, 0, x, method, steps, &o.seg_sc);
+  o.c = mirror_proposed(c_table, 1, x, method, steps, &o.seg_sc);
+  o.t = mirror_proposed(c_table, 2, x, method, steps, &o.seg_t);
+  return o;
+}
+
 // Fused proposed sin/cos/tan of one element (kernels.hpp:46-67).  SEG: also
 // produce both segment choices even for functions not in MASK.
+//
+// Row choice: g = floor(red * 12/pi) from one fma.rz, validated by
+// klo <= red < khi (and the same for the tan angle, which differs from the
+// sin/cos one by a few ulps at most, so it shares the row).  A lane fails the
+// check only near a knot, at red == +0, for the r < 0 / r >= period cases the
+// reference clamps, or for non-finite x -- it then recomputes the element with
+// the exact device restatement (mirror_*), so every lane returns the
+// reference's bits.
 template <int SQ, unsigned MASK, bool SEG = false>
 __device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, int steps) {
   constexpr bool kSC = (MASK & (kSin | kCos)) != 0 || SEG;
   constexpr bool kT = (MASK & kTan) != 0 || SEG;
-  const FastRed fr = fast_reduce<kSC, kT>(x);
+  const FastConsts& K = c_fast;
+  const FastRed fr = fast_reduce<kSC, kT, false>(x);
+  const double key = kSC ? fr.red : fr.redt;
+  const unsigned g = static_cast<unsigned>(__double2loint(__fma_rz(key, K.twelve_over_pi, K.two52))) & 7u;
+  const SegRow& s = tb.row[g];
+  bool ok = true;
+  if constexpr (kSC) ok = fr.red >= s.klo && fr.red < s.khi;
+  if constexpr (kT) ok = ok && fr.redt >= s.klo && fr.redt < s.khi;
   Out3 o{0.0, 0.0, 0.0, 0, 0};
   if constexpr (kSC) {
-    const unsigned off = seg_off(fr.red);
-    if constexpr (SEG) o.seg_sc = static_cast<int>(off / kRowBytes);
-    const SegRow& s = row_at(tb, off);
     const double red = fr.red;
     const double rad = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(s.X, red), s.Y), red), s.Z);
     const double rs = fast_rsqrt<SQ>(rad, steps);
@@ -423,9 +467,6 @@ __device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, int
       o.c = xor_hi(__dmul_rn(__dadd_rn(__dmul_rn(s.c, red), s.d), rs), fr.neg_c);
   }
   if constexpr (kT) {
-    const unsigned off = seg_off(fr.redt);
-    if constexpr (SEG) o.seg_t = fr.guard ? 255 : static_cast<int>(off / kRowBytes);
-    const SegRow& s = row_at(tb, off);
     const double red = fr.redt;
     const double poly = __dadd_rn(__dmul_rn(s.a, red), s.b);
     const double den = __dadd_rn(__dmul_rn(s.c, red), s.d);
@@ -439,6 +480,11 @@ __device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, int
     v = fr.guard ? __longlong_as_double(0x7ff0000000000000ll) : v;
     o.t = xor_hi(v, fr.neg_t);
   }
+  if constexpr (SEG) {
+    o.seg_sc = s.seg;
+    o.seg_t = fr.guard ? 255 : s.seg;
+  }
+  if (!ok) o = slow_proposed(x, SQ == kExact ? 0 : 1, SQ == kFisr1 ? 1 : steps);  // rare
   return o;
 }
 
@@ -463,7 +509,7 @@ template <int NT, unsigned MASK>
 __device__ __forceinline__ Out3 fast_taylor(double x, int n) {
   constexpr bool kSC = (MASK & (kSin | kCos)) != 0;
   constexpr bool kT = (MASK & kTan) != 0;
-  const FastRed fr = fast_reduce<kSC, kT>(x);
+  const FastRed fr = fast_reduce<kSC, kT, true>(x);
   Out3 o{0.0, 0.0, 0.0, 0, 0};
   if constexpr (kSC) {
     const double s2 = __dmul_rn(fr.red, fr.red);

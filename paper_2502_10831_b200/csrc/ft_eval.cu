@@ -13,7 +13,7 @@ namespace {
 
 constexpr int kThreads = 256;
 #ifndef FT_MINB
-#define FT_MINB 6  // __launch_bounds__ min blocks per SM for K1/K2 (<= 40 registers)
+#define FT_MINB 5  // __launch_bounds__ min blocks per SM for K1/K2 (<= 48 registers, no spills)
 #endif
 
 template <typename T>
