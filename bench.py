@@ -286,7 +286,6 @@ def run_ours(args) -> None:
     # ---- accuracy: K3 over the whole shard, NCCL-reduced (max / sum)
     st = ft.parity_reduce(x, out, w.mask, kind=w.kind, mode=mode, n_terms=w.n_terms, ulp_tol=2)
     st = reduce_stats(st, device=dev)  # the path's only collective: 64 B of stats
-    nf = max(1, sum(st["n_finite_libm"]))
     accuracy = {
         "checked": int(st["n_checked"]), "max_ulp_vs_oracle": st["max_ulp"],
         "over_2ulp": st["n_over_tol"],
@@ -296,7 +295,6 @@ def run_ours(args) -> None:
         "nan_count": st["n_nan"], "checksum": st["checksum"], "outputs": names,
         "oracle": "device restatement of the reference (ft_mirror_*), bitwise-pinned to the CPU oracle",
     }
-    del nf
 
     # ---- e2e through the public host-pointer C-ABI call (pinned host buffers)
     e2e = None
