@@ -12,11 +12,7 @@ namespace ft {
 namespace {
 
 constexpr int kThreads = 256;
-#ifndef FT_WS
-#define FT_WS 0  // >0: K1/K2 use the warp-specialised TMA-store map with FT_WS ring slots
-#endif
-// K1/K2 block: kThreads compute threads (+ one store warp when FT_WS).
-constexpr int kK12Threads = kThreads + (FT_WS > 0 ? 32 : 0);
+constexpr int kK12Threads = kThreads;
 #ifndef FT_MINB
 #define FT_MINB 5  // __launch_bounds__ min blocks per SM for K1/K2 (<= 48 registers, no spills)
 #endif
@@ -44,57 +40,6 @@ template <>
 __device__ __forceinline__ float to_out<float>(double v) { return __double2float_rn(v); }
 template <>
 __device__ __forceinline__ double to_out<double>(double v) { return v; }
-
-__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(m));
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// TMA bulk load of `bytes` into smem; completion counted on mbarrier m.
-__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, unsigned bytes,
-                                          unsigned long long* m) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
-  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(m));
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
-      "l"(gsrc), "r"(bytes), "r"(b)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned phase) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(m));
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(phase)
-      : "memory");
-}
-
-// TMA bulk store smem -> global (SASS UBLKCP), bulk-group completion.
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-// Make this thread's generic-proxy smem writes visible to the async (TMA) proxy.
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* m) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(m));
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_read_all() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
 
 // The streaming map shared by every evaluation kernel.  `op(double) -> Out3`.
 template <typename T, unsigned MASK, bool SEG, class Op>
@@ -154,108 +99,6 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
 }
 
 
-// Warp-specialised variant of stream_map for K1/K2 (blockDim = kThreads + 32).
-// Warps 0..7 evaluate (x by direct 16-byte loads, as in stream_map) and write
-// each tile's outputs to a shared-memory ring; warp 8 (the store warp) issues
-// one TMA bulk store per output array per 4 KiB tile.  Hand-off is two
-// mbarriers per ring slot (full: 8 warp arrivals; empty: the store warp's
-// arrival once TMA has read the slot), so compute warps never meet a block
-// barrier.  Bulk stores issue the write-heavy stream at 97.7% of the copy roof
-// against 85.6% for per-thread stores (tools/stream_variants.cu).
-template <typename T, unsigned MASK, class Op>
-__device__ __forceinline__ void stream_map_ws(const EvalArgs& a, const Op& op) {
-  using V = Vec<T>;
-  using VT = typename V::type;
-  constexpr int VN = V::N;
-  constexpr int NB = FT_WS;  // ring slots
-  constexpr unsigned kTileBytes = kThreads * sizeof(VT);
-  const T* __restrict__ x = static_cast<const T*>(a.x);
-  T* __restrict__ o0 = static_cast<T*>(a.out[0]);
-  T* __restrict__ o1 = static_cast<T*>(a.out[1]);
-  T* __restrict__ o2 = static_cast<T*>(a.out[2]);
-  const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto eval = [&](const VT& xin, VT res[3]) {
-    T xs[VN], rs[VN], rc[VN], rt[VN];
-    V::unpack(xin, xs);
-#pragma unroll
-    for (int j = 0; j < VN; ++j) {
-      const Out3 o = op(static_cast<double>(xs[j]));
-      rs[j] = to_out<T>(o.s);
-      rc[j] = to_out<T>(o.c);
-      rt[j] = to_out<T>(o.t);
-    }
-    res[0] = V::pack(rs);
-    res[1] = V::pack(rc);
-    res[2] = V::pack(rt);
-  };
-  std::size_t done = 0;
-  if (a.vec_ok) {
-    const std::size_t nv = a.n / VN;
-    const VT* __restrict__ xv = reinterpret_cast<const VT*>(x);
-    const std::size_t nt = nv / kThreads;
-    __shared__ __align__(128) VT ring[NB][3][kThreads];
-    __shared__ __align__(8) unsigned long long full[NB], empty[NB];
-    if (threadIdx.x == 0) {
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        mbar_init(&full[b], kThreads / 32);
-        mbar_init(&empty[b], 1);
-      }
-      fence_mbar_init();
-    }
-    __syncthreads();
-    if (warp < kThreads / 32) {
-      unsigned i = 0;
-      for (std::size_t t = blockIdx.x; t < nt; t += gridDim.x, ++i) {
-        const unsigned b = i % NB, ph = (i / NB) & 1u;
-        VT res[3];
-        eval(__ldcs(xv + t * kThreads + threadIdx.x), res);
-        mbar_wait(&empty[b], ph ^ 1u);  // slot drained by TMA (passes at once on round 0)
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          if (MASK & (1u << j)) ring[b][j][threadIdx.x] = res[j];
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[b]);
-      }
-      // partial tile: direct stores
-      for (std::size_t v = nt * kThreads + blockIdx.x * static_cast<std::size_t>(kThreads) + threadIdx.x;
-           v < nv; v += static_cast<std::size_t>(gridDim.x) * kThreads) {
-        VT res[3];
-        eval(__ldcs(xv + v), res);
-        if constexpr ((MASK & kSin) != 0) __stcs(reinterpret_cast<VT*>(o0) + v, res[0]);
-        if constexpr ((MASK & kCos) != 0) __stcs(reinterpret_cast<VT*>(o1) + v, res[1]);
-        if constexpr ((MASK & kTan) != 0) __stcs(reinterpret_cast<VT*>(o2) + v, res[2]);
-      }
-    } else if (lane == 0) {  // store warp
-      unsigned i = 0;
-      for (std::size_t t = blockIdx.x; t < nt; t += gridDim.x, ++i) {
-        const unsigned b = i % NB, ph = (i / NB) & 1u;
-        mbar_wait(&full[b], ph);
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          if (MASK & (1u << j))
-            bulk_store(reinterpret_cast<VT*>(j == 0 ? o0 : j == 1 ? o1 : o2) + t * kThreads,
-                       &ring[b][j][0], kTileBytes);
-        bulk_commit();
-        bulk_wait_read_all();
-        mbar_arrive(&empty[b]);
-      }
-      bulk_wait_all();
-    }
-    done = nv * VN;
-  }
-  if (threadIdx.x < kThreads) {
-    for (std::size_t i = done + blockIdx.x * static_cast<std::size_t>(kThreads) + threadIdx.x; i < a.n;
-         i += static_cast<std::size_t>(gridDim.x) * kThreads) {
-      const Out3 o = op(static_cast<double>(x[i]));
-      if constexpr ((MASK & kSin) != 0) o0[i] = to_out<T>(o.s);
-      if constexpr ((MASK & kCos) != 0) o1[i] = to_out<T>(o.c);
-      if constexpr ((MASK & kTan) != 0) o2[i] = to_out<T>(o.t);
-    }
-  }
-}
-
 template <int SQ, unsigned MASK, bool SEG>
 struct ProposedOp {
   const SmemTable* tb;
@@ -300,15 +143,13 @@ __global__ void __launch_bounds__(kK12Threads, FT_MINB) k_proposed(const EvalArg
   __shared__ SmemTable tb;
   stage_table(&tb);
   __syncthreads();
-  if constexpr (FT_WS > 0 && !SEG) stream_map_ws<T, MASK>(a, ProposedOp<SQ, MASK, SEG>{&tb, a.steps});
-  else stream_map<T, MASK, SEG>(a, ProposedOp<SQ, MASK, SEG>{&tb, a.steps});
+  stream_map<T, MASK, SEG>(a, ProposedOp<SQ, MASK, SEG>{&tb, a.steps});
 }
 
 // ---------------- K2 ----------------
 template <typename T, int NT, unsigned MASK>
 __global__ void __launch_bounds__(kK12Threads, FT_MINB) k_taylor(const EvalArgs a) {
-  if constexpr (FT_WS > 0) stream_map_ws<T, MASK>(a, TaylorOp<NT, MASK>{a.steps});
-  else stream_map<T, MASK, false>(a, TaylorOp<NT, MASK>{a.steps});
+  stream_map<T, MASK, false>(a, TaylorOp<NT, MASK>{a.steps});
 }
 
 // ---------------- device restatement ----------------
