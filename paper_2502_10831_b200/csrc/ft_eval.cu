@@ -13,8 +13,11 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kK12Threads = kThreads;
+#ifndef FT_RPF
+#define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
+#endif
 #ifndef FT_MINB
-#define FT_MINB 5  // __launch_bounds__ min blocks per SM for K1/K2 (<= 48 registers, no spills)
+#define FT_MINB 4  // __launch_bounds__ min blocks per SM for K1/K2 (<= 64 registers, no spills)
 #endif
 
 template <typename T>
@@ -82,7 +85,23 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
         }
       }
     };
+#if FT_RPF
+    // Register prefetch: the next iteration's x is loaded before this one is
+    // evaluated, so its DRAM latency (reads queue behind the write stream)
+    // overlaps the arithmetic.  With 4 blocks/SM (<= 64 registers) this beat
+    // direct loads, cp.async / TMA staging, L2 prefetch hints and prefetching
+    // two iterations ahead (profiles/r01_k1_variants.json).
+    VT cur{};
+    if (tid < nv) cur = __ldcs(xv + tid);
+    for (std::size_t v = tid; v < nv; v += stride) {
+      VT nxt{};
+      if (v + stride < nv) nxt = __ldcs(xv + v + stride);
+      body(cur, v);
+      cur = nxt;
+    }
+#else
     for (std::size_t v = tid; v < nv; v += stride) body(__ldcs(xv + v), v);
+#endif
 
     done = nv * VN;
   }

@@ -160,7 +160,42 @@ void run(const char* name, KF f, int blocks_per_sm, double2* x, double2* o[3], s
   printf("{\"variant\": \"%s\", \"blocks_per_sm\": %d, \"ms\": %.4f, \"gbs\": %.1f}\n", name, bps, t * 1e3, bytes / t / 1e9);
 }
 
-int main() {
+void sustained(const char* name, KF f, int bps, double2* x, double2* o[3], size_t nv, float seconds) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  dim3 grid(sms * bps);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  f<<<grid, 256>>>(x, o[0], o[1], o[2], nv);
+  cudaDeviceSynchronize();
+  int reps = 0;
+  float ms = 0;
+  cudaEventRecord(e0);
+  while (ms < seconds * 1000) {
+    for (int r = 0; r < 50; ++r) f<<<grid, 256>>>(x, o[0], o[1], o[2], nv);
+    reps += 50;
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+  }
+  const double t = ms / reps * 1e-3, bytes = double(nv) * 16 * 4;
+  printf("{\"variant\": \"%s sustained %.1fs\", \"blocks_per_sm\": %d, \"ms\": %.4f, \"gbs\": %.1f}\n", name, seconds, bps,
+         t * 1e3, bytes / t / 1e9);
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1) {  // sustained mode: ~3 s per kernel (nvidia-smi samples power/clocks alongside)
+    const size_t bytes = size_t(2) << 30, nv = bytes / 16;
+    double2 *x, *o[3];
+    cudaMalloc(&x, bytes);
+    for (auto& p : o) cudaMalloc(&p, bytes);
+    cudaMemset(x, 0, bytes);
+    sustained("v0 grid-stride .cs", v0, 5, x, o, nv, 3.0f);
+    sustained("v4 tma bulk store", v4, 5, x, o, nv, 3.0f);
+    return 0;
+  }
+
   const size_t bytes = size_t(2) << 30, nv = bytes / 16;
   double2 *x, *o[3];
   cudaMalloc(&x, bytes);
