@@ -17,7 +17,8 @@ synchronize on both sides, max over ranks.
 
 `e2e` is the same metric through the public host-pointer C-ABI call
 (ft_proposed_batch_host) with pinned host buffers: every step copies x in and
-sin/cos/tan out.  `cpu_baseline` (rank 0, N=1) and `--impl reference` time the
+sin/cos/tan out (2^26 elements per rank per step by default, so N ranks pin
+N x 2 GiB of host memory, not N x 8 GiB; the rate is PCIe-bound either way).  `cpu_baseline` (rank 0, N=1) and `--impl reference` time the
 reference's own CPU implementation (oracle/_ref: the unmodified reference
 headers, all host threads) on a bounded sample of the same workload.
 """
@@ -304,7 +305,7 @@ def run_ours(args) -> None:
     # ---- e2e through the public host-pointer C-ABI call (pinned host buffers)
     e2e = None
     if not args.no_e2e:
-        n_e2e = min(n, args.e2e_elements or n)
+        n_e2e = min(n, args.e2e_elements)
         xh = torch.empty(n_e2e, dtype=tdt, pin_memory=True)
         xh.copy_(x[:n_e2e])
         outs_h = {nm: torch.empty(n_e2e, dtype=tdt, pin_memory=True) for nm in names}
@@ -392,7 +393,8 @@ def main() -> None:
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--elements", type=int, default=0, help="override elements per GPU")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-elements", type=int, default=0)
+    ap.add_argument("--e2e-elements", type=int, default=1 << 26,
+                    help="elements per rank per e2e step (pinned host buffers of this size)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
