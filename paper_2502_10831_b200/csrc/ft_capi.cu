@@ -3,9 +3,10 @@
 // Argument validation, status codes and a thread-local error string; the
 // host-pointer batch entry points (the reference's std::span -> std::vector
 // API, R:proj/include/fasttrig/kernels.hpp:84-94) as a chunked H2D / K1 / D2H
-// pipeline over three streams; grid sizing; the once-per-process threshold
-// search that lets K1 replace two divisions and a compare chain by integer-
-// ordered compares.
+// pipeline over three streams; grid sizing; the host bisection that derives
+// the fast path's quadrant / pole-guard thresholds from IEEE division and
+// subtraction (their compiled-in copies must match it bit for bit, see
+// ft_thresholds and tests/test_capi_host.py).
 #include <algorithm>
 #include <atomic>
 #include <cmath>

@@ -25,7 +25,11 @@
 //                 compare (monotone in red on [0, pi/2]);
 //               * sign multiplications by +-1.0 as sign-bit XORs and 0.5*v as
 //                 an exponent decrement (both exact for the values they see);
-//               * no clamp of red and no isfinite branch (see fast_reduce).
+//               * the segment row from one fma.rz guess validated by a bracket
+//                 compare, shared by tan; elements the bracket cannot certify
+//                 (near knots, the reference's r clamps, +0, NaN) are redone
+//                 by the mirror path -- so no r / red clamp and no isfinite
+//                 branch on the fast path (see fast_proposed).
 //             All products/sums that the reference rounds separately stay
 //             separately rounded.
 #pragma once

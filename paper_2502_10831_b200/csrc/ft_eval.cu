@@ -12,7 +12,6 @@ namespace ft {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kK12Threads = kThreads;
 #ifndef FT_RPF
 #define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
 #endif
@@ -158,7 +157,7 @@ struct MirrorOp {
 
 // ---------------- K1 ----------------
 template <typename T, int SQ, unsigned MASK, bool SEG>
-__global__ void __launch_bounds__(kK12Threads, FT_MINB) k_proposed(const EvalArgs a) {
+__global__ void __launch_bounds__(kThreads, FT_MINB) k_proposed(const EvalArgs a) {
   __shared__ SmemTable tb;
   stage_table(&tb);
   __syncthreads();
@@ -167,7 +166,7 @@ __global__ void __launch_bounds__(kK12Threads, FT_MINB) k_proposed(const EvalArg
 
 // ---------------- K2 ----------------
 template <typename T, int NT, unsigned MASK>
-__global__ void __launch_bounds__(kK12Threads, FT_MINB) k_taylor(const EvalArgs a) {
+__global__ void __launch_bounds__(kThreads, FT_MINB) k_taylor(const EvalArgs a) {
   stream_map<T, MASK, false>(a, TaylorOp<NT, MASK>{a.steps});
 }
 
@@ -178,7 +177,7 @@ __global__ void __launch_bounds__(kThreads) k_mirror(const EvalArgs a, int kind,
 }
 
 template <class K>
-cudaError_t go(K kernel, const EvalArgs& a, cudaStream_t s, int threads = kK12Threads) {
+cudaError_t go(K kernel, const EvalArgs& a, cudaStream_t s, int threads = kThreads) {
   const unsigned blocks = persistent_blocks(reinterpret_cast<const void*>(kernel), threads, a.n);
   kernel<<<blocks, threads, 0, s>>>(a);
   count_launch();
