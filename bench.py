@@ -228,7 +228,8 @@ def run_ours(args) -> None:
         print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # torchrun
+    if world > 1 or launched:
         dist.init_process_group("nccl", device_id=dev)
     _lib.lib()  # fail loudly if the CUDA library is missing
 
@@ -255,7 +256,7 @@ def run_ours(args) -> None:
             ft.taylor_eval(x, w.n_terms, w.mask, out=out)
 
     def barrier():
-        if world > 1:
+        if dist.is_initialized():
             dist.barrier()
 
     for _ in range(max(args.warmup, 3)):
@@ -379,7 +380,7 @@ def run_ours(args) -> None:
             "accuracy": accuracy,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 
