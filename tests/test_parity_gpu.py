@@ -294,3 +294,27 @@ def test_launch_counter_counts_kernels(ft):
     ft.taylor_eval(x, 5, 3)
     torch.cuda.synchronize()
     assert ft.launch_count() - before == 3
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_no_out_of_bounds_writes(ft, dtype):
+    """compute-sanitizer is closed on this pool, so bounds are checked directly:
+    every output (and the segment arrays) is a view into a larger buffer filled
+    with a canary; after K1 / K2 / K4 the canary outside each view is intact."""
+    guard = 4099
+    canary = -12345.678 if dtype == torch.float64 else -1234.5
+    for n in (1, 3, 17, 4096, 20011):
+        for off in (0, 1, 2):
+            x = ft.gen_inputs(n + off, dtype, 0, -500.0, 500.0, 11)[off:]
+            bufs = {nm: torch.full((n + 2 * guard + off,), canary, dtype=dtype, device="cuda")
+                    for nm in ("sin", "cos", "tan")}
+            views = {nm: b[guard + off: guard + off + n] for nm, b in bufs.items()}
+            ft.proposed_eval(x, 7, out=views)
+            ft.taylor_eval(x, 5, 7, out=views)
+            gbuf = torch.full((n + 2 * guard + off,), canary, dtype=dtype, device="cuda")
+            ft.gen_inputs(n, dtype, 0, 0.0, 1.0, 3, out=gbuf[guard + off: guard + off + n])
+            torch.cuda.synchronize()
+            for b in list(bufs.values()) + [gbuf]:
+                h = b.cpu().numpy()
+                assert np.all(h[: guard + off] == np.array(canary, h.dtype)), (n, off)
+                assert np.all(h[guard + off + n:] == np.array(canary, h.dtype)), (n, off)
