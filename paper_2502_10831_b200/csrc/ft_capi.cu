@@ -13,7 +13,9 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
+#include <vector>
 
 #include "ft_internal.h"
 
@@ -165,6 +167,77 @@ int pipe_reserve(HostPipe& p, std::size_t bytes) {
   return FT_OK;
 }
 
+// Pageable host memory (e.g. the std::vector the reference API returns) goes
+// through a pinned staging ring: parallel host memcpys into / out of pinned
+// slots, overlapped with the H2D / kernel / D2H streams of other chunks.
+constexpr std::size_t kStageChunk = std::size_t(1) << 21;  // elements per staged chunk
+struct Staging {
+  void* pin[kPipe][4]{};  // x, sin, cos, tan
+  cudaEvent_t done[kPipe]{};
+  std::size_t cap_bytes = 0;
+};
+Staging g_stage[128];
+
+bool host_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice ||
+         at.type == cudaMemoryTypeManaged;
+}
+
+int stage_reserve(Staging& g, std::size_t bytes) {
+  if (!g.done[0]) {
+    for (auto& e : g.done) {
+      cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      if (r != cudaSuccess) return cuda_status(r, "cudaEventCreate");
+    }
+  }
+  if (bytes <= g.cap_bytes) return FT_OK;
+  for (auto& row : g.pin)
+    for (auto& b : row) {
+      if (b) cudaFreeHost(b);
+      b = nullptr;
+    }
+  g.cap_bytes = 0;
+  for (auto& row : g.pin)
+    for (auto& b : row) {
+      cudaError_t r = cudaHostAlloc(&b, bytes, cudaHostAllocDefault);
+      if (r != cudaSuccess) return cuda_status(r, "cudaHostAlloc(staging)");
+    }
+  g.cap_bytes = bytes;
+  return FT_OK;
+}
+
+// A batch of memcpys split into ~4 MiB parts over up to 16 host threads (one
+// core moves ~10 GB/s; the staged path needs ~32 B per element through memory).
+struct Copy {
+  void* dst;
+  const void* src;
+  std::size_t bytes;
+};
+void parallel_copies(const std::vector<Copy>& copies) {
+  const std::size_t part = std::size_t(4) << 20;
+  std::vector<Copy> parts;
+  for (const Copy& c : copies)
+    for (std::size_t lo = 0; lo < c.bytes; lo += part)
+      parts.push_back({static_cast<char*>(c.dst) + lo, static_cast<const char*>(c.src) + lo,
+                       std::min(part, c.bytes - lo)});
+  if (parts.empty()) return;
+  unsigned hw = std::thread::hardware_concurrency();
+  const std::size_t nt = std::min<std::size_t>({16, hw ? hw : 1, parts.size()});
+  auto work = [&](std::size_t t) {
+    for (std::size_t i = t; i < parts.size(); i += nt) std::memcpy(parts[i].dst, parts[i].src, parts[i].bytes);
+  };
+  std::vector<std::thread> th;
+  for (std::size_t t = 1; t < nt; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& t : th) t.join();
+}
+
 // Chunked H2D -> kernel -> D2H over kPipe streams.  `launch(args, stream)`.
 template <class Launch>
 int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* const out[3],
@@ -178,6 +251,64 @@ int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* 
   int rc = pipe_reserve(p, chunk * es);
   if (rc) return rc;
   const char* xb = static_cast<const char*>(x);
+  const bool x_pinned = host_pinned(x);
+  bool o_pinned = true;
+  for (int j = 0; j < 3; ++j) o_pinned = o_pinned && (!(mask & (1u << j)) || host_pinned(out[j]));
+  if (!x_pinned || !o_pinned) {
+    // ---- staged path for pageable buffers ----
+    Staging& g = g_stage[dev];
+    if ((rc = stage_reserve(g, kStageChunk * es))) return rc;
+    struct Pending {
+      bool live = false;
+      std::size_t off = 0, m = 0;
+    } pend[kPipe];
+    // Wait for slot k's previous chunk; queue the copy of its outputs to the user.
+    auto retire = [&](int k, std::vector<Copy>& copies) -> int {
+      if (!pend[k].live) return FT_OK;
+      cudaError_t e = cudaEventSynchronize(g.done[k]);
+      if (e != cudaSuccess) return cuda_status(e, "cudaEventSynchronize");
+      if (!o_pinned)
+        for (int j = 0; j < 3; ++j)
+          if (mask & (1u << j))
+            copies.push_back({static_cast<char*>(out[j]) + pend[k].off * es, g.pin[k][1 + j], pend[k].m * es});
+      pend[k].live = false;
+      return FT_OK;
+    };
+    std::size_t ci = 0;
+    for (std::size_t off = 0; off < n; off += kStageChunk, ++ci) {
+      const int k = static_cast<int>(ci % kPipe);
+      const std::size_t m = std::min(kStageChunk, n - off);
+      std::vector<Copy> copies;
+      if ((rc = retire(k, copies))) return rc;  // slot k is free once its last chunk is out
+      const void* src = xb + off * es;
+      if (!x_pinned) {
+        copies.push_back({g.pin[k][0], src, m * es});
+        src = g.pin[k][0];
+      }
+      parallel_copies(copies);  // previous outputs out and this input in, together
+      cudaStream_t s = p.st[k];
+      cudaError_t e = cudaMemcpyAsync(p.buf[k][0], src, m * es, cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync H2D");
+      void* dout[3] = {p.buf[k][1], p.buf[k][2], p.buf[k][3]};
+      e = launch(p.buf[k][0], m, dout, s);
+      if (e != cudaSuccess) return cuda_status(e, "kernel launch");
+      for (int j = 0; j < 3; ++j) {
+        if (!(mask & (1u << j))) continue;
+        void* dst = o_pinned ? static_cast<char*>(out[j]) + off * es : g.pin[k][1 + j];
+        e = cudaMemcpyAsync(dst, dout[j], m * es, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync D2H");
+      }
+      e = cudaEventRecord(g.done[k], s);
+      if (e != cudaSuccess) return cuda_status(e, "cudaEventRecord");
+      pend[k] = {true, off, m};
+    }
+    for (std::size_t i = 0; i < static_cast<std::size_t>(kPipe); ++i) {  // oldest first
+      std::vector<Copy> copies;
+      if ((rc = retire(static_cast<int>((ci + i) % kPipe), copies))) return rc;
+      parallel_copies(copies);
+    }
+    return FT_OK;
+  }
   std::size_t ci = 0;
   for (std::size_t off = 0; off < n; off += chunk, ++ci) {
     const int k = static_cast<int>(ci % kPipe);
