@@ -144,6 +144,28 @@ def cpu_rate(get_x, mask: int, threads: int, target_s: float, kind_pref: str = "
     return x.size / dt / 1e9, kind, x.size, dt, x
 
 
+def api_single_thread_rate(w, n: int = 1 << 20):
+    """The reference's own batch API, exactly as a caller uses it (R:kernels.hpp:84-94:
+    one thread, allocates a std::vector per call), for sin, cos and tan in turn.
+    Returns Gelem/s of fused-equivalent work (elements / total time of the 3 calls)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        return None
+    x = O.gen_uniform(n, w.lo, w.hi, w.seed, 0, np.float64)
+    out = np.empty_like(x)
+    R = O.ref()
+    best = float("inf")
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for which in range(3):
+            R.ref_api_batch(which, x.ctypes.data, n, 1, 1, out.ctypes.data)
+        best = min(best, time.perf_counter() - t0)
+    return n / best / 1e9
+
+
 def host_inputs(w):
     """Host copy of the first n elements of workload w's input stream (uniform
     configs are generated on the host bit-identically to K4)."""
@@ -202,7 +224,8 @@ def run_reference(args) -> None:
         "vs_baseline": None, "dtype": "f64" if w.itemsize == 8 else "f32", "data": "synthetic",
         "config": {"workload": w.name, "description": w.note, "elements_per_step": n},
         "cpu_baseline": {"value": round(value, 6), "unit": "Gelem/s", "cores": threads,
-                         "kind": kind, "sample": sample},
+                         "kind": kind, "sample": sample,
+                         "api_batch_single_thread_gelem_s": api_single_thread_rate(w)},
         "e2e": {"value": round(value, 6), "unit": "Gelem/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -354,7 +377,8 @@ def run_ours(args) -> None:
         cpu = {"value": round(rate, 6), "unit": "Gelem/s", "cores": threads, "kind": kind,
                "sample": f"first {ns} elements of this workload ({sec:.1f} s, one run); fused "
                          f"sin+cos+tan via the scalar reference calls over {threads} threads; "
-                         f"{host_cpu_model()}"}
+                         f"{host_cpu_model()}",
+               "api_batch_single_thread_gelem_s": api_single_thread_rate(w)}
 
     if rank == 0:
         line = {
