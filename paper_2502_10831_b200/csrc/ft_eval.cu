@@ -49,18 +49,21 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
   using V = Vec<T>;
   using VT = typename V::type;
   constexpr int VN = V::N;
-  const std::size_t tid = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
-  const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
+  // 32-bit indices: each launch covers < 2^31 elements (launch_* split larger
+  // arrays), so addresses are one IMAD.WIDE.U32 each instead of 64-bit math.
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned stride = gridDim.x * blockDim.x;
+  const unsigned n = static_cast<unsigned>(a.n);
   const T* __restrict__ x = static_cast<const T*>(a.x);
   T* __restrict__ o0 = static_cast<T*>(a.out[0]);
   T* __restrict__ o1 = static_cast<T*>(a.out[1]);
   T* __restrict__ o2 = static_cast<T*>(a.out[2]);
-  std::size_t done = 0;
+  unsigned done = 0;
   if (a.vec_ok) {
-    const std::size_t nv = a.n / VN;
+    const unsigned nv = n / VN;
     const VT* __restrict__ xv = reinterpret_cast<const VT*>(x);
     // Evaluate + store one vector.
-    auto body = [&](const VT& xin, std::size_t v) {
+    auto body = [&](const VT& xin, unsigned v) {
       T xs[VN], rs[VN], rc[VN], rt[VN];
       std::uint8_t g0[VN], g1[VN];
       V::unpack(xin, xs);
@@ -92,19 +95,19 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
     // two iterations ahead (profiles/r01_k1_variants.json).
     VT cur{};
     if (tid < nv) cur = __ldcs(xv + tid);
-    for (std::size_t v = tid; v < nv; v += stride) {
+    for (unsigned v = tid; v < nv; v += stride) {
       VT nxt{};
       if (v + stride < nv) nxt = __ldcs(xv + v + stride);
       body(cur, v);
       cur = nxt;
     }
 #else
-    for (std::size_t v = tid; v < nv; v += stride) body(__ldcs(xv + v), v);
+    for (unsigned v = tid; v < nv; v += stride) body(__ldcs(xv + v), v);
 #endif
 
     done = nv * VN;
   }
-  for (std::size_t i = done + tid; i < a.n; i += stride) {
+  for (unsigned i = done + tid; i < n; i += stride) {
     const Out3 o = op(static_cast<double>(x[i]));
     if constexpr ((MASK & kSin) != 0) o0[i] = to_out<T>(o.s);
     if constexpr ((MASK & kCos) != 0) o1[i] = to_out<T>(o.c);
@@ -246,27 +249,53 @@ cudaError_t taylor_dt(unsigned mask, int n_terms, const EvalArgs& a, cudaStream_
   }
 }
 
+// Split launches so every kernel sees < 2^31 elements (32-bit indexing); the
+// offsets keep 16-byte alignment.
+constexpr std::size_t kMaxLaunch = std::size_t(1) << 30;
+
+template <class F>
+cudaError_t chunked(ft_dtype dt, const EvalArgs& a, F&& launch_one) {
+  if (a.n <= kMaxLaunch) return launch_one(a);
+  const std::size_t es = dt == FT_F32 ? 4 : 8;
+  for (std::size_t off = 0; off < a.n; off += kMaxLaunch) {
+    EvalArgs b = a;
+    b.n = std::min(kMaxLaunch, a.n - off);
+    b.x = static_cast<const char*>(a.x) + off * es;
+    for (int j = 0; j < 3; ++j)
+      if (a.out[j]) b.out[j] = static_cast<char*>(a.out[j]) + off * es;
+    if (a.seg_sc) b.seg_sc = a.seg_sc + off;
+    if (a.seg_t) b.seg_t = a.seg_t + off;
+    const cudaError_t e = launch_one(b);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace
 
 cudaError_t launch_proposed(ft_dtype dt, unsigned mask, int sq, bool seg, const EvalArgs& a,
                             cudaStream_t s) {
-  return dt == FT_F32 ? proposed_dt<float>(mask, sq, seg, a, s)
-                      : proposed_dt<double>(mask, sq, seg, a, s);
+  return chunked(dt, a, [&](const EvalArgs& b) {
+    return dt == FT_F32 ? proposed_dt<float>(mask, sq, seg, b, s) : proposed_dt<double>(mask, sq, seg, b, s);
+  });
 }
 
 cudaError_t launch_taylor(ft_dtype dt, unsigned mask, int n_terms, const EvalArgs& a,
                           cudaStream_t s) {
   EvalArgs b = a;
   b.steps = n_terms;  // Taylor kernels read the term count from `steps`
-  return dt == FT_F32 ? taylor_dt<float>(mask, n_terms, b, s) : taylor_dt<double>(mask, n_terms, b, s);
+  return chunked(dt, b, [&](const EvalArgs& c) {
+    return dt == FT_F32 ? taylor_dt<float>(mask, n_terms, c, s) : taylor_dt<double>(mask, n_terms, c, s);
+  });
 }
 
 cudaError_t launch_mirror(ft_dtype dt, unsigned mask, int kind, int method, int n_terms,
                           const EvalArgs& a, cudaStream_t s) {
   EvalArgs b = a;
   if (kind == 1) b.steps = n_terms;
-  return dt == FT_F32 ? mirror_t<float>(mask, b, kind, method, s)
-                      : mirror_t<double>(mask, b, kind, method, s);
+  return chunked(dt, b, [&](const EvalArgs& c) {
+    return dt == FT_F32 ? mirror_t<float>(mask, c, kind, method, s) : mirror_t<double>(mask, c, kind, method, s);
+  });
 }
 
 }  // namespace ft

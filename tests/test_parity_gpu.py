@@ -318,3 +318,23 @@ def test_no_out_of_bounds_writes(ft, dtype):
                 h = b.cpu().numpy()
                 assert np.all(h[: guard + off] == np.array(canary, h.dtype)), (n, off)
                 assert np.all(h[guard + off + n:] == np.array(canary, h.dtype)), (n, off)
+
+
+def test_arrays_longer_than_one_launch(ft):
+    """Launches are split at 2^30 elements (32-bit in-kernel indexing): results
+    on both sides of every split point equal the oracle and the launch count
+    reflects the split."""
+    n = (1 << 30) + 4099
+    w = CONFIGS["cfg5"]
+    xd = ft.gen_inputs(n, torch.float32, 0, w.lo, w.hi, w.seed, 77)
+    before = ft.launch_count()
+    out = ft.proposed_eval(xd, 7)
+    torch.cuda.synchronize()
+    assert ft.launch_count() - before == 2
+    for lo, hi in ((0, 4096), ((1 << 30) - 4096, n)):
+        x = host(xd[lo:hi])
+        ref = O.proposed(x, 7)
+        for f in ref:
+            assert same_bits(host(out[f][lo:hi]), ref[f]), (lo, f)
+    st = ft.parity_reduce(xd, out, 7, ulp_tol=ULP_TOL)
+    assert st["n_checked"] == n and st["max_ulp"] == [0, 0, 0]
