@@ -271,20 +271,20 @@ __device__ __forceinline__ double mirror_taylor(const TaylorCoeffs& C, int which
 // fast_*: production path (bitwise equal to mirror_* for every input)
 // ======================================================================
 //
-// Instruction budget is the design constraint (an FP64-heavy elementwise map
-// is issue-bound before it is HBM-bound on B200), so:
-//   * every constant is a kernel parameter (read as a c[0x0][] operand, never
-//     re-materialised into registers inside the loop);
-//   * compares are DSETP (one issue slot, exact) and their predicates feed
-//     SELs directly -- no integer quadrant / segment numbers are formed;
+// Instruction count (and, at the power cap, energy) per element is the design
+// constraint, so:
+//   * every constant lives in constant bank 3 (c_fast) and is read as a c[][]
+//     instruction operand, never re-materialised into registers in the loop;
+//   * compares are DSETP (one issue slot, exact) whose predicates feed SELs
+//     directly -- no integer quadrant number is formed;
 //   * the quadrant fold is one DADD of a selected base and a sign-selected r
 //     (reference: {r, pi-r, r-pi, 2pi-r}); the reference's final clamp of red
 //     to [0, pi/2] is provably a no-op once r is in [0, 2pi)
-//     (tests/test_capi_host.py::test_fold_needs_no_clamp checks the quadrant
-//     edges), so it is not executed;
-//   * non-finite x needs no branch: the r clamp is written so NaN survives it
-//     (ordered compares are false for NaN), every later step propagates NaN,
-//     and all segment compares fail (segment 0, like the reference).
+//     (tests/test_capi_host.py::test_fold_needs_no_clamp checks the edges);
+//   * the reference's r clamps are not executed either: an r outside
+//     [0, period) folds to red <= 0 or NaN, which fails the row bracket of
+//     fast_proposed and sends the element to the exact path -- so non-finite
+//     x needs no branch of its own.
 
 // Per-segment coefficient row in shared memory: the coefficients plus the
 // half-open bracket [klo, khi) of reduced angles the row is valid for.
