@@ -70,13 +70,17 @@ def ncu_traffic(workload: str):
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap,power.draw,clocks.mem")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+
+    def mark(self):
+        """Samples taken before the last mark() are dropped (idle / setup)."""
+        self.t_mark = time.time()
 
     def start(self):
         try:
@@ -86,7 +90,8 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
-        time.sleep(0.3)  # let the first sample land before the timed region
+        self.t_mark = 0.0
+        time.sleep(0.2)  # let nvidia-smi start sampling
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -99,20 +104,25 @@ class ClockSampler:
             out = ""
         sm, smax, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        import datetime
+
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 8:
                 continue
             try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                if ts < self.t_mark:
+                    continue
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[3:7]):
+            for nm, v in zip(names, parts[4:8]):
                 if v.lower() == "active":
                     reasons.add(nm)
             try:
-                pw.append(float(parts[7]))
+                pw.append(float(parts[8]))
             except (ValueError, IndexError):
                 pass
         if not sm:
@@ -282,12 +292,12 @@ def run_ours(args) -> None:
         if dist.is_initialized():
             dist.barrier()
 
+    clocks = ClockSampler(local)  # samples from warm-up start to timed-region end (GPU loaded)
+    clocks.start()
+    clocks.mark()
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
-
-    clocks = ClockSampler(local)
-    clocks.start()
     barrier()
     torch.cuda.synchronize()
     l0 = ft.launch_count()

@@ -287,7 +287,7 @@ int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* 
       }
       parallel_copies(copies);  // previous outputs out and this input in, together
       cudaStream_t s = p.st[k];
-      cudaError_t e = cudaMemcpyAsync(p.buf[k][0], src, m * es, cudaMemcpyHostToDevice, s);
+      cudaError_t e = cudaMemcpyAsync(p.buf[k][0], src, m * es, cudaMemcpyDefault, s);
       if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync H2D");
       void* dout[3] = {p.buf[k][1], p.buf[k][2], p.buf[k][3]};
       e = launch(p.buf[k][0], m, dout, s);
@@ -295,7 +295,7 @@ int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* 
       for (int j = 0; j < 3; ++j) {
         if (!(mask & (1u << j))) continue;
         void* dst = o_pinned ? static_cast<char*>(out[j]) + off * es : g.pin[k][1 + j];
-        e = cudaMemcpyAsync(dst, dout[j], m * es, cudaMemcpyDeviceToHost, s);
+        e = cudaMemcpyAsync(dst, dout[j], m * es, cudaMemcpyDefault, s);
         if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync D2H");
       }
       e = cudaEventRecord(g.done[k], s);
@@ -314,7 +314,7 @@ int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* 
     const int k = static_cast<int>(ci % kPipe);
     const std::size_t m = std::min(chunk, n - off);
     cudaStream_t s = p.st[k];
-    cudaError_t e = cudaMemcpyAsync(p.buf[k][0], xb + off * es, m * es, cudaMemcpyHostToDevice, s);
+    cudaError_t e = cudaMemcpyAsync(p.buf[k][0], xb + off * es, m * es, cudaMemcpyDefault, s);
     if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync H2D");
     void* dout[3] = {p.buf[k][1], p.buf[k][2], p.buf[k][3]};
     e = launch(p.buf[k][0], m, dout, s);
@@ -322,7 +322,7 @@ int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* 
     for (int j = 0; j < 3; ++j) {
       if (!(mask & (1u << j))) continue;
       e = cudaMemcpyAsync(static_cast<char*>(out[j]) + off * es, dout[j], m * es,
-                          cudaMemcpyDeviceToHost, s);
+                          cudaMemcpyDefault, s);
       if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync D2H");
     }
   }
