@@ -142,13 +142,13 @@ struct MirrorOp {
   int kind, method, steps, n;
   __device__ __forceinline__ Out3 operator()(double x) const {
     Out3 o{0.0, 0.0, 0.0, 0, 0};
-    int seg = 0;
     if (kind == 0) {
-      if (MASK & kSin) o.s = mirror_proposed(c_table, 0, x, method, steps, &seg);
-      if (MASK & kCos) o.c = mirror_proposed(c_table, 1, x, method, steps, &seg);
-      (void)mirror_proposed(c_table, 0, x, method, steps, &o.seg_sc);
-      o.t = mirror_proposed(c_table, 2, x, method, steps, &o.seg_t);
-      if (!(MASK & kTan)) o.t = 0.0;
+      int seg_cos = 0;
+      const double s = mirror_proposed(c_table, 0, x, method, steps, &o.seg_sc);
+      if (MASK & kSin) o.s = s;
+      if (MASK & kCos) o.c = mirror_proposed(c_table, 1, x, method, steps, &seg_cos);
+      const double t = mirror_proposed(c_table, 2, x, method, steps, &o.seg_t);
+      if (MASK & kTan) o.t = t;
     } else {
       if (MASK & kSin) o.s = mirror_taylor(c_taylor, 0, x, n);
       if (MASK & kCos) o.c = mirror_taylor(c_taylor, 1, x, n);

@@ -338,3 +338,21 @@ def test_arrays_longer_than_one_launch(ft):
             assert same_bits(host(out[f][lo:hi]), ref[f]), (lo, f)
     st = ft.parity_reduce(xd, out, 7, ulp_tol=ULP_TOL)
     assert st["n_checked"] == n and st["max_ulp"] == [0, 0, 0]
+
+
+@pytest.mark.parametrize("mode", list(MODES) + ["fisr3"])
+def test_host_batch_api_every_sqrt_mode(ft, mode):
+    """The reference-shaped host API (kernels.hpp:84-94) in every SqrtMode, f64 and
+    f32, on the golden edge cases: bitwise equal to the oracle."""
+    m, s = MODES.get(mode, (1, 3))
+    sm = ft.SqrtMode(m, s)
+    x = np.concatenate([np.linspace(-20, 20, 40001), [0.0, -0.0, np.inf, -np.inf, np.nan, 1e300, -1e-310]])
+    ref = O.proposed(x, 7, m, s)
+    assert same_bits(ft.proposed_sin_batch(x, sm), ref["sin"])
+    assert same_bits(ft.proposed_cos_batch(x, sm), ref["cos"])
+    assert same_bits(ft.proposed_tan_batch(x, sm), ref["tan"])
+    xf = x.astype(np.float32)
+    r = ft.proposed_batch(xf, 7, sm)
+    ref = O.proposed(xf, 7, m, s)
+    for f in ref:
+        assert same_bits(r[f], ref[f]), f
