@@ -55,15 +55,33 @@ def peaks() -> tuple[float, str]:
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload: str):
-    """Per-launch DRAM bytes of K1 from the committed ncu --set full summary, if any."""
+def ncu_summary() -> dict:
+    """The committed ncu --set full summary of K1/K2 (profiles/ncu_k1_summary.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_k1_summary.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d.get("traffic_bytes_per_launch", {}).get(workload)
+            return json.load(f)
     except Exception:
+        return {}
+
+
+def ncu_traffic(workload: str):
+    """Per-launch DRAM bytes of K1 from the committed ncu --set full summary, if any."""
+    return ncu_summary().get("traffic_bytes_per_launch", {}).get(workload)
+
+
+def fp64_roof(workload: str, gelem_s_per_gpu: float):
+    """The FP64-pipe roof beside the HBM one: issued FP64-pipe instructions per
+    element (ncu, this kernel) x throughput vs the measured DFMA lane-op peak."""
+    d = ncu_summary()
+    ops = d.get("fp64_pipe_instr_per_elem", {}).get(workload)
+    peak = d.get("fp64_peak_lane_ops_per_s")
+    if not ops or not peak:
         return None
+    ach = ops * gelem_s_per_gpu * 1e9
+    return {"bound": "fp64", "ops_per_elem": ops, "achieved": round(ach / 1e12, 3),
+            "peak": round(peak / 1e12, 3), "unit": "T lane-ops/s", "frac": round(ach / peak, 4),
+            "source": "ops/elem from profiles/ncu_k1_summary.json; peak " + d.get("fp64_peak_source", "")}
 
 
 # ------------------------------------------------------------------ clocks
@@ -407,6 +425,7 @@ def run_ours(args) -> None:
                          "traffic": ncu_traffic(w.name), "peak_source": peak_src,
                          "algorithmic_bytes_per_elem": w.bytes_per_elem,
                          "kernel": "k_proposed (K1)" if w.kind == 0 else "k_taylor (K2)"},
+            "fp64_roof": fp64_roof(w.name, n / (ms / 1e3) / 1e9),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
