@@ -12,11 +12,20 @@ namespace ft {
 namespace {
 
 constexpr int kThreads = 256;
+// Output path per dtype.  f64 (32 B/elem at cfg2, memory-bound): block tiles
+// written by TMA bulk stores at 3 blocks/SM -- equal to per-thread stores
+// under the sustained power cap and 12% faster per launch (6.16 vs 5.51 TB/s).
+// f32 (16 B/elem, instruction-bound): per-thread streaming stores at 4 blocks/SM
+// (the TMA path costs it 3-5%).  profiles/r01_k1_variants.json.
+#ifndef FT_TMA_F64
+#define FT_TMA_F64 1
+#endif
+template <typename T>
+constexpr bool kTmaStores = sizeof(T) == 8 && FT_TMA_F64;
+template <typename T>
+constexpr int kMinBlocks = kTmaStores<T> ? 3 : 4;
 #ifndef FT_RPF
 #define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
-#endif
-#ifndef FT_MINB
-#define FT_MINB 4  // __launch_bounds__ min blocks per SM for K1/K2 (<= 64 registers, no spills)
 #endif
 
 template <typename T>
@@ -43,6 +52,21 @@ __device__ __forceinline__ float to_out<float>(double v) { return __double2float
 template <>
 __device__ __forceinline__ double to_out<double>(double v) { return v; }
 
+// TMA bulk store smem -> global (SASS UBLKCP) and its bulk-group completion.
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // The streaming map shared by every evaluation kernel.  `op(double) -> Out3`.
 template <typename T, unsigned MASK, bool SEG, class Op>
 __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
@@ -63,7 +87,8 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
     const unsigned nv = n / VN;
     const VT* __restrict__ xv = reinterpret_cast<const VT*>(x);
     // Evaluate + store one vector.
-    auto body = [&](const VT& xin, unsigned v) {
+    // Evaluate one vector into res[] (+ segment bytes in the SEG variant).
+    auto compute = [&](const VT& xin, unsigned v, VT res[3]) {
       T xs[VN], rs[VN], rc[VN], rt[VN];
       std::uint8_t g0[VN], g1[VN];
       V::unpack(xin, xs);
@@ -76,9 +101,9 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
         g0[j] = static_cast<std::uint8_t>(o.seg_sc);
         g1[j] = static_cast<std::uint8_t>(o.seg_t);
       }
-      if constexpr ((MASK & kSin) != 0) __stcs(reinterpret_cast<VT*>(o0) + v, V::pack(rs));
-      if constexpr ((MASK & kCos) != 0) __stcs(reinterpret_cast<VT*>(o1) + v, V::pack(rc));
-      if constexpr ((MASK & kTan) != 0) __stcs(reinterpret_cast<VT*>(o2) + v, V::pack(rt));
+      res[0] = V::pack(rs);
+      res[1] = V::pack(rc);
+      res[2] = V::pack(rt);
       if constexpr (SEG) {
 #pragma unroll
         for (int j = 0; j < VN; ++j) {
@@ -87,6 +112,51 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
         }
       }
     };
+    // Evaluate + store one vector with per-thread 16-byte streaming stores.
+    auto body = [&](const VT& xin, unsigned v) {
+      VT res[3];
+      compute(xin, v, res);
+      if constexpr ((MASK & kSin) != 0) __stcs(reinterpret_cast<VT*>(o0) + v, res[0]);
+      if constexpr ((MASK & kCos) != 0) __stcs(reinterpret_cast<VT*>(o1) + v, res[1]);
+      if constexpr ((MASK & kTan) != 0) __stcs(reinterpret_cast<VT*>(o2) + v, res[2]);
+    };
+    if constexpr (kTmaStores<T> && !SEG) {
+      // Block tiles of kThreads vectors; x register-prefetched one tile ahead;
+      // outputs staged in a 3-slot shared-memory ring and written by one
+      // thread as one TMA bulk store per output array per tile.  One barrier
+      // per tile: after issuing tile i, thread 0 waits until the bulk store of
+      // tile i-1 has read its slot; the next barrier publishes that to every
+      // thread before the slot is refilled (tile i+2).
+      __shared__ __align__(128) VT stage[3][3][kThreads];
+      const unsigned nt = nv / kThreads;
+      unsigned t = blockIdx.x;
+      VT cur{};
+      if (t < nt) cur = __ldcs(xv + t * kThreads + threadIdx.x);
+      unsigned slot = 0;
+      for (; t < nt; t += gridDim.x, slot = slot == 2 ? 0 : slot + 1) {
+        VT nxt{};
+        if (t + gridDim.x < nt) nxt = __ldcs(xv + (t + gridDim.x) * kThreads + threadIdx.x);
+        VT res[3];
+        compute(cur, t * kThreads + threadIdx.x, res);
+        cur = nxt;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          if (MASK & (1u << j)) stage[slot][j][threadIdx.x] = res[j];
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (MASK & (1u << j))
+              bulk_store(reinterpret_cast<VT*>(j == 0 ? o0 : j == 1 ? o1 : o2) + t * kThreads,
+                         &stage[slot][j][0], kThreads * sizeof(VT));
+          bulk_commit();
+          bulk_wait_read_1();  // tile i-1's slot is free once the next barrier passes
+        }
+      }
+      for (unsigned v = nt * kThreads + tid; v < nv; v += stride) body(__ldcs(xv + v), v);
+      if (threadIdx.x == 0) bulk_wait_all();
+    } else {
 #if FT_RPF
     // Register prefetch: the next iteration's x is loaded before this one is
     // evaluated, so its DRAM latency (reads queue behind the write stream)
@@ -104,6 +174,7 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
 #else
     for (unsigned v = tid; v < nv; v += stride) body(__ldcs(xv + v), v);
 #endif
+    }
 
     done = nv * VN;
   }
@@ -160,7 +231,7 @@ struct MirrorOp {
 
 // ---------------- K1 ----------------
 template <typename T, int SQ, unsigned MASK, bool SEG>
-__global__ void __launch_bounds__(kThreads, FT_MINB) k_proposed(const EvalArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_proposed(const EvalArgs a) {
   __shared__ SmemTable tb;
   stage_table(&tb);
   __syncthreads();
@@ -169,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, FT_MINB) k_proposed(const EvalArgs a
 
 // ---------------- K2 ----------------
 template <typename T, int NT, unsigned MASK>
-__global__ void __launch_bounds__(kThreads, FT_MINB) k_taylor(const EvalArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_taylor(const EvalArgs a) {
   stream_map<T, MASK, false>(a, TaylorOp<NT, MASK>{a.steps});
 }
 
