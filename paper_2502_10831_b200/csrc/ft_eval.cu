@@ -20,10 +20,15 @@ constexpr int kThreads = 256;
 #ifndef FT_TMA_F64
 #define FT_TMA_F64 1
 #endif
+#ifndef FT_TMA_TAYLOR_F32
+#define FT_TMA_TAYLOR_F32 0
+#endif
 template <typename T>
-constexpr bool kTmaStores = sizeof(T) == 8 && FT_TMA_F64;
+constexpr bool kTmaK1 = sizeof(T) == 8 && FT_TMA_F64;
 template <typename T>
-constexpr int kMinBlocks = kTmaStores<T> ? 3 : 4;
+constexpr bool kTmaK2 = (sizeof(T) == 8 && FT_TMA_F64) || (sizeof(T) == 4 && FT_TMA_TAYLOR_F32);
+template <typename T>
+constexpr int kMinBlocks = kTmaK1<T> ? 3 : 4;
 #ifndef FT_RPF
 #define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
 #endif
@@ -68,7 +73,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 // The streaming map shared by every evaluation kernel.  `op(double) -> Out3`.
-template <typename T, unsigned MASK, bool SEG, class Op>
+template <typename T, unsigned MASK, bool SEG, class Op, bool TMA = false>
 __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
   using V = Vec<T>;
   using VT = typename V::type;
@@ -120,7 +125,7 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
       if constexpr ((MASK & kCos) != 0) __stcs(reinterpret_cast<VT*>(o1) + v, res[1]);
       if constexpr ((MASK & kTan) != 0) __stcs(reinterpret_cast<VT*>(o2) + v, res[2]);
     };
-    if constexpr (kTmaStores<T> && !SEG) {
+    if constexpr (TMA && !SEG) {
       // Block tiles of kThreads vectors; x register-prefetched one tile ahead;
       // outputs staged in a 3-slot shared-memory ring and written by one
       // thread as one TMA bulk store per output array per tile.  One barrier
@@ -235,13 +240,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_proposed(const Eval
   __shared__ SmemTable tb;
   stage_table(&tb);
   __syncthreads();
-  stream_map<T, MASK, SEG>(a, ProposedOp<SQ, MASK, SEG>{&tb, a.steps});
+  stream_map<T, MASK, SEG, ProposedOp<SQ, MASK, SEG>, kTmaK1<T>>(a, ProposedOp<SQ, MASK, SEG>{&tb, a.steps});
 }
 
 // ---------------- K2 ----------------
 template <typename T, int NT, unsigned MASK>
 __global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_taylor(const EvalArgs a) {
-  stream_map<T, MASK, false>(a, TaylorOp<NT, MASK>{a.steps});
+  stream_map<T, MASK, false, TaylorOp<NT, MASK>, kTmaK2<T>>(a, TaylorOp<NT, MASK>{a.steps});
 }
 
 // ---------------- device restatement ----------------
