@@ -357,3 +357,24 @@ def test_host_batch_api_every_sqrt_mode(ft, mode):
     ref = O.proposed(xf, 7, m, s)
     for f in ref:
         assert same_bits(r[f], ref[f]), f
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_random_bit_patterns_full_range(ft, dtype):
+    """2^26 uniformly random bit patterns (every exponent and sign, incl. subnormals,
+    huge arguments, NaN/inf) through K1, checked by K3 against the device
+    restatement (itself bitwise-pinned to the CPU oracle) in every SqrtMode."""
+    n = 1 << 26
+    gen = torch.Generator(device="cuda").manual_seed(1234)
+    if dtype == torch.float64:
+        bits = torch.randint(-(2**63), 2**63 - 1, (n,), dtype=torch.int64, device="cuda", generator=gen)
+    else:
+        bits = torch.randint(-(2**31), 2**31 - 1, (n,), dtype=torch.int32, device="cuda", generator=gen)
+    x = bits.view(dtype)
+    for m, s in ((1, 1), (0, 0), (1, 2)):
+        mode = ft.SqrtMode(m, s)
+        out = ft.proposed_eval(x, 7, mode, seg=True)
+        st = ft.parity_reduce(x, out, 7, mode=mode, ulp_tol=ULP_TOL, check_seg=True)
+        assert st["n_checked"] == n
+        assert st["max_ulp"] == [0, 0, 0], (m, s, st["max_ulp"])
+        assert st["seg_mismatch"] == [0, 0]
