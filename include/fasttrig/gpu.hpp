@@ -61,6 +61,11 @@ constexpr ft_dtype dtype_of() {
   return std::is_same_v<T, float> ? FT_F32 : FT_F64;
 }
 
+// How many GPUs one host-memory call spreads over (default 1; n <= 0: all
+// visible).  Arrays of >= 4 Mi elements are split into contiguous shards, one
+// device and host thread each; results do not depend on the setting.
+inline void set_devices(int n) { check(ft_set_host_devices(n)); }
+
 // ---- reference-shaped batch calls (host memory in, host memory out) ----
 inline std::vector<double> proposed_sin_batch(std::span<const double> xs, SqrtMode mode = {}) {
   std::vector<double> out(xs.size());

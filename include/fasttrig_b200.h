@@ -105,6 +105,14 @@ int ft_proposed_batch_host(ft_dtype dtype, const void* x, size_t n, unsigned mas
 int ft_taylor_batch_host(ft_dtype dtype, const void* x, size_t n, unsigned mask, int n_terms,
                          void* sin_out, void* cos_out, void* tan_out);
 
+/* Number of GPUs the host-pointer entry points spread one call over: arrays of
+ * at least 4 Mi elements are split into that many contiguous shards, each
+ * streamed through its own device (round robin from the current one) by its
+ * own host thread.  Default 1 (the current device); n <= 0 selects every
+ * visible device.  Results are identical for any setting. */
+int ft_set_host_devices(int n);
+int ft_get_host_devices(void);
+
 /* ---- device-pointer entry points (asynchronous on `stream`) ---- */
 
 /* K1: fused proposed sin/cos/tan (kernels.hpp:46-67 per element). */

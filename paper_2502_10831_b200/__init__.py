@@ -11,6 +11,7 @@ from .fasttrig import (  # noqa: F401
     TAN,
     SqrtMode,
     gen_inputs,
+    get_host_devices,
     l2_flush,
     launch_count,
     mirror_eval,
@@ -21,6 +22,7 @@ from .fasttrig import (  # noqa: F401
     proposed_sin_batch,
     proposed_tan_batch,
     segment_table,
+    set_host_devices,
     taylor_batch,
     taylor_coeffs,
     taylor_eval,

@@ -27,6 +27,7 @@ EXPORTS = (
     "ft_taylor_eval", "ft_mirror_eval", "ft_parity_reduce", "ft_stats_reset", "ft_gen_inputs",
     "ft_l2_flush", "ft_host_alloc", "ft_host_free", "ft_segment_table", "ft_taylor_coeffs",
     "ft_thresholds", "ft_launch_count", "ft_last_error_string", "ft_abi_version",
+    "ft_set_host_devices", "ft_get_host_devices",
 )
 
 
@@ -102,6 +103,7 @@ def lib() -> C.CDLL:
             "ft_segment_table": [vp],
             "ft_taylor_coeffs": [vp, vp, vp],
             "ft_thresholds": [vp],
+            "ft_set_host_devices": [i32],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -113,6 +115,8 @@ def lib() -> C.CDLL:
         L.ft_last_error_string.argtypes = []
         L.ft_abi_version.restype = C.c_int
         L.ft_abi_version.argtypes = []
+        L.ft_get_host_devices.restype = C.c_int
+        L.ft_get_host_devices.argtypes = []
         _lib = L
         return L
 

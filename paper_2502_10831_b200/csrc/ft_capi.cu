@@ -335,6 +335,52 @@ int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* 
   return FT_OK;
 }
 
+// ---- host-pointer calls over several GPUs ----
+// ft_set_host_devices(G): host-pointer calls split arrays of at least
+// kMinShard elements into G contiguous shards, one per device (round robin from
+// the current device), each streamed by its own host thread through that
+// device's pipeline -- every GPU brings its own PCIe link.  G <= 0: all visible.
+std::atomic<int> g_host_devices{1};
+constexpr std::size_t kMinShard = std::size_t(1) << 22;
+
+template <class Launch>
+int host_sharded(int dtype, const void* x, std::size_t n, unsigned mask, void* const out[3],
+                 Launch&& launch) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    (void)cudaGetLastError();
+    return fail(FT_ERR_NO_DEVICE, "no CUDA device visible");
+  }
+  int want = g_host_devices.load();
+  if (want <= 0) want = ndev;
+  const std::size_t G = std::min<std::size_t>(static_cast<std::size_t>(want), std::max<std::size_t>(1, n / kMinShard));
+  if (G <= 1) return host_pipeline(dtype, x, n, mask, out, launch);
+  const std::size_t es = dtype == FT_F32 ? 4 : 8;
+  const int base = current_device();
+  std::vector<int> rcs(G, FT_OK);
+  std::vector<std::string> errs(G);
+  std::vector<std::thread> th;
+  for (std::size_t g = 0; g < G; ++g) {
+    const std::size_t lo = n * g / G, hi = n * (g + 1) / G;
+    th.emplace_back([&, g, lo, hi] {
+      cudaError_t e = cudaSetDevice(static_cast<int>((base + g) % static_cast<std::size_t>(ndev)));
+      if (e != cudaSuccess) {
+        rcs[g] = cuda_status(e, "cudaSetDevice");
+        errs[g] = g_err;
+        return;
+      }
+      void* o[3];
+      for (int j = 0; j < 3; ++j) o[j] = out[j] ? static_cast<char*>(out[j]) + lo * es : nullptr;
+      rcs[g] = host_pipeline(dtype, static_cast<const char*>(x) + lo * es, hi - lo, mask, o, launch);
+      if (rcs[g]) errs[g] = g_err;  // g_err is per thread
+    });
+  }
+  for (auto& t : th) t.join();
+  for (std::size_t g = 0; g < G; ++g)
+    if (rcs[g]) return fail(rcs[g], errs[g]);
+  return FT_OK;
+}
+
 // ---- L2 flush buffer (per device) ----
 struct FlushBuf {
   std::mutex mu;
@@ -534,6 +580,13 @@ int ft_l2_flush(void* stream) {
   return cuda_status(launch_fill(f.p, f.bytes, ++f.tick, as_stream(stream)), "ft_l2_flush");
 }
 
+int ft_set_host_devices(int n) {
+  g_host_devices.store(n);
+  return FT_OK;
+}
+
+int ft_get_host_devices(void) { return g_host_devices.load(); }
+
 int ft_host_alloc(void** p, size_t bytes) {
   if (!p) return fail(FT_ERR_INVALID_ARG, "p is NULL");
   return cuda_status(cudaHostAlloc(p, bytes, cudaHostAllocDefault), "cudaHostAlloc");
@@ -549,7 +602,7 @@ int ft_proposed_batch_host(ft_dtype dtype, const void* x, size_t n, unsigned mas
   if ((rc = check_mode(mode))) return rc;
   if (n == 0) return FT_OK;
   const int sq = sqrt_kind(mode);
-  return host_pipeline(dtype, x, n, mask, out,
+  return host_sharded(dtype, x, n, mask, out,
                        [&](const void* dx, std::size_t m, void* const dout[3], cudaStream_t s) {
                          EvalArgs a = make_args(dx, m, mask, dout, nullptr, nullptr, mode.newton_steps);
                          return launch_proposed(dtype, mask, sq, false, a, s);
@@ -563,7 +616,7 @@ int ft_taylor_batch_host(ft_dtype dtype, const void* x, size_t n, unsigned mask,
   if (rc) return rc;
   if (n_terms < 1 || n_terms > 9) return fail(FT_ERR_INVALID_ARG, "n_terms must be in [1, 9]");
   if (n == 0) return FT_OK;
-  return host_pipeline(dtype, x, n, mask, out,
+  return host_sharded(dtype, x, n, mask, out,
                        [&](const void* dx, std::size_t m, void* const dout[3], cudaStream_t s) {
                          EvalArgs a = make_args(dx, m, mask, dout, nullptr, nullptr, n_terms);
                          return launch_taylor(dtype, mask, n_terms, a, s);

@@ -234,5 +234,14 @@ def thresholds() -> np.ndarray:
     return out
 
 
+def set_host_devices(n: int) -> None:
+    """How many GPUs one host-pointer call spreads over (n <= 0: all visible)."""
+    L.check(L.lib().ft_set_host_devices(n))
+
+
+def get_host_devices() -> int:
+    return int(L.lib().ft_get_host_devices())
+
+
 def launch_count() -> int:
     return int(L.lib().ft_launch_count())

@@ -121,3 +121,10 @@ def test_fold_needs_no_clamp(ft):
     assert 0.0 <= T2 - pi and prev(T3) - pi <= hp           # q=2: red = r - pi
     assert 0.0 <= tp - prev(tp) and tp - T3 <= hp           # q=3: red = 2pi - r
     assert 0.0 <= pi - prev(pi) and pi - nxt(hp) <= hp      # tan upper: red = pi - r
+
+
+def test_host_device_setting_roundtrip(ft):
+    assert ft.get_host_devices() == 1  # default: the current device only
+    ft.set_host_devices(0)
+    assert ft.get_host_devices() == 0
+    ft.set_host_devices(1)

@@ -378,3 +378,30 @@ def test_random_bit_patterns_full_range(ft, dtype):
         assert st["n_checked"] == n
         assert st["max_ulp"] == [0, 0, 0], (m, s, st["max_ulp"])
         assert st["seg_mismatch"] == [0, 0]
+
+
+@pytest.mark.parametrize("devices", [2, 3, 0])
+def test_host_api_sharded_over_devices(ft, devices):
+    """ft_set_host_devices: one host call split into shards, one host thread and
+    device pipeline each (on a single-GPU box the shards share the device), both
+    for pinned and pageable buffers; bitwise equal to the oracle."""
+    w = CONFIGS["cfg2"]
+    n = (1 << 24) + 12345
+    x = O.gen_uniform(n, w.lo, w.hi, w.seed, 0)
+    ref = O.proposed(x, 7)
+    try:
+        ft.set_host_devices(devices)
+        r = ft.proposed_batch(x, 7)  # pageable numpy buffers
+        for f in ref:
+            assert same_bits(r[f], ref[f]), f
+        xp = torch.from_numpy(x).pin_memory()
+        outs = {f: torch.empty(n, dtype=torch.float64, pin_memory=True).numpy() for f in ref}
+        ft.proposed_batch(xp.numpy(), 7, out=outs)
+        for f in ref:
+            assert same_bits(outs[f], ref[f]), f
+        t = ft.taylor_batch(x.astype(np.float32), 5, 3)
+        tr = O.taylor(x.astype(np.float32), 5, 3)
+        for f in tr:
+            assert same_bits(t[f], tr[f]), f
+    finally:
+        ft.set_host_devices(1)
