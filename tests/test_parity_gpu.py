@@ -405,3 +405,51 @@ def test_host_api_sharded_over_devices(ft, devices):
             assert same_bits(t[f], tr[f]), f
     finally:
         ft.set_host_devices(1)
+
+
+def test_concurrent_callers(ft):
+    """Several host threads on their own streams, mixing device-pointer and
+    host-pointer calls at the same time (the C ABI's occupancy cache, launch
+    counter, host pipelines and error strings are shared state)."""
+    import threading
+
+    w = CONFIGS["cfg2"]
+    x = O.gen_uniform(1 << 20, w.lo, w.hi, w.seed, 4242)
+    ref = O.proposed(x, 7)
+    xd = dev(x)
+    errors = []
+
+    def device_worker(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(5):
+                    out = ft.proposed_eval(xd, 7, stream=s)
+                    s.synchronize()
+                    for f in ref:
+                        assert same_bits(host(out[f]), ref[f])
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    def host_worker(k):
+        try:
+            for _ in range(3):
+                r = ft.proposed_batch(x, 7)
+                for f in ref:
+                    assert same_bits(r[f], ref[f])
+                bad = None
+                try:
+                    ft.taylor_batch(x, 99, 3)
+                except Exception as e:  # noqa: BLE001
+                    bad = str(e)
+                assert bad and "n_terms" in bad  # this thread's own error text
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=device_worker, args=(k,)) for k in range(4)]
+    th += [threading.Thread(target=host_worker, args=(k,)) for k in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
