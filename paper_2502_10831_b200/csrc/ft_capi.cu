@@ -123,7 +123,7 @@ EvalArgs make_args(const void* x, std::size_t n, unsigned mask, void* const out[
 
 int sqrt_kind(ft_sqrt_mode m) {
   if (m.method == FT_SQRT_EXACT) return kExact;
-  return m.newton_steps == 1 ? kFisr1 : kFisrN;
+  return m.newton_steps == 1 ? kFisr1 : m.newton_steps == 2 ? kFisr2 : kFisrN;
 }
 
 int check_mode(ft_sqrt_mode m) {

@@ -134,7 +134,7 @@ constexpr FastConsts make_fast_consts() {
 constexpr FastConsts kFast = make_fast_consts();
 
 // Sqrt-mode selector as a template parameter of the kernels.
-enum SqrtKind : int { kExact = 0, kFisr1 = 1, kFisrN = 2 };
+enum SqrtKind : int { kExact = 0, kFisr1 = 1, kFisrN = 2, kFisr2 = 3 };  // kFisrN: runtime step count
 
 // Output mask bits (mirrors include/fasttrig_b200.h).
 enum : unsigned { kSin = 1u, kCos = 2u, kTan = 4u };
@@ -357,8 +357,9 @@ __device__ __forceinline__ double fast_rsqrt(double v, int steps) {
                                   static_cast<unsigned long long>(__funnelshift_r(lo, hi, 1));
     double y = u2d(kFisrMagic - sh);
     const double half_v = __hiloint2double(static_cast<int>(hi - 0x00100000u), static_cast<int>(lo));
-    if constexpr (SQ == kFisr1) {
+    if constexpr (SQ == kFisr1 || SQ == kFisr2) {
       y = __dmul_rn(y, __dsub_rn(1.5, __dmul_rn(__dmul_rn(half_v, y), y)));
+      if constexpr (SQ == kFisr2) y = __dmul_rn(y, __dsub_rn(1.5, __dmul_rn(__dmul_rn(half_v, y), y)));
     } else {
       for (int i = 0; i < steps; ++i)
         y = __dmul_rn(y, __dsub_rn(1.5, __dmul_rn(__dmul_rn(half_v, y), y)));
@@ -488,7 +489,7 @@ __device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, int
     o.seg_sc = s.seg;
     o.seg_t = fr.guard ? 255 : s.seg;
   }
-  if (!ok) o = slow_proposed(x, SQ == kExact ? 0 : 1, SQ == kFisr1 ? 1 : steps);  // rare
+  if (!ok) o = slow_proposed(x, SQ == kExact ? 0 : 1, SQ == kFisr1 ? 1 : SQ == kFisr2 ? 2 : steps);  // rare
   return o;
 }
 

@@ -305,12 +305,14 @@ cudaError_t proposed_dt(unsigned mask, int sq, bool seg, const EvalArgs& a, cuda
     switch (sq) {
       case kExact: return proposed_t<T, kExact, true>(mask, a, s);
       case kFisr1: return proposed_t<T, kFisr1, true>(mask, a, s);
+      case kFisr2: return proposed_t<T, kFisr2, true>(mask, a, s);
       default: return proposed_t<T, kFisrN, true>(mask, a, s);
     }
   }
   switch (sq) {
     case kExact: return proposed_t<T, kExact, false>(mask, a, s);
     case kFisr1: return proposed_t<T, kFisr1, false>(mask, a, s);
+    case kFisr2: return proposed_t<T, kFisr2, false>(mask, a, s);
     default: return proposed_t<T, kFisrN, false>(mask, a, s);
   }
 }
