@@ -1,7 +1,7 @@
 #!/bin/bash
 # Collect the round's GPU evidence with the default in-tree build.
 # Usage (under gpurun): bash tools/round_evidence.sh <tag>
-tag=${1:-r01d}
+tag=${1:-r01f}
 out=gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()" > $out/${tag}_smoke.log 2>&1; echo "smoke rc=$?"
 python bench.py > $out/${tag}_bench.json 2> $out/${tag}_bench.err; echo "bench rc=$?"
