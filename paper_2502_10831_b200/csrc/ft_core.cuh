@@ -29,7 +29,12 @@
 //                 compare, shared by tan; elements the bracket cannot certify
 //                 (near knots, the reference's r clamps, +0, NaN) are redone
 //                 by the mirror path -- so no r / red clamp and no isfinite
-//                 branch on the fast path (see fast_proposed).
+//                 branch on the fast path (see fast_proposed);
+//               * the quadrant / tan-fold compares and the bracket on the
+//                 high words only (integer pipe): an r sharing a threshold's
+//                 high word may fold wrongly, but then lands in no bracket;
+//               * 2*q1 as an exponent increment, the FISR Newton step as
+//                 y*fma(-0.5, (v*y)*y, 1.5) (same roundings, see fisr_newton).
 //             All products/sums that the reference rounds separately stay
 //             separately rounded.
 #pragma once
@@ -124,12 +129,13 @@ struct FastConsts {
   double pi, two_pi, half_pi, inv_two_pi;
   double twelve_over_pi;  // RN(12/pi): row guess floor(red * 12/pi)
   double two52;           // 2^52: fma.rz(red, 12/pi, 2^52) puts floor() in the low word
+  double half;            // 0.5 (FISR Newton step, as a c[][] operand)
 };
 constexpr FastConsts make_fast_consts() {
   return FastConsts{{kHalfPi, kPi, 3.0 * kHalfPi},
                     0x1.91de2c0cf70aep+0,
                     {kTable.knots[1], kTable.knots[2], kTable.knots[3], kTable.knots[4], kTable.knots[5]},
-                    kPi, kTwoPi, kHalfPi, kInvTwoPi, 12.0 / kPi, 0x1p52};
+                    kPi, kTwoPi, kHalfPi, kInvTwoPi, 12.0 / kPi, 0x1p52, 0.5};
 }
 constexpr FastConsts kFast = make_fast_consts();
 
@@ -287,36 +293,51 @@ __device__ __forceinline__ double mirror_taylor(const TaylorCoeffs& C, int which
 //     x needs no branch of its own.
 
 // Per-segment coefficient row in shared memory: the coefficients plus the
-// half-open bracket [klo, khi) of reduced angles the row is valid for.
+// bracket of reduced angles the row is valid for, as the high words of its two
+// ends: a lane accepts the row iff klo_hi < hi(red) < khi_hi (signed compare).
+// That implies knot_lo < red < knot_hi for any red (negative and NaN red have
+// a negative or > inf high word and never pass), and it is what lets the
+// quadrant compares of fast_reduce use high words only (see there).
 // 80-byte stride: the 16-byte chunks of the eight rows fall in disjoint banks
 // (80k/4 mod 32 = 0,20,8,28,16,4,24,12), so a warp's LDS.128 never conflicts
 // whichever rows its lanes pick.
 struct alignas(16) SegRow {
   double a, b, c, d, X, Y, Z;
-  double klo, khi;
-  int seg, pad;
+  int klo_hi, khi_hi;  // 16-byte chunk with Z
+  double klo, khi;     // exact bracket [klo, khi) (tan-only kernels)
 };
 constexpr unsigned kRowBytes = sizeof(SegRow);
 static_assert(kRowBytes == 80, "row stride");
 
+// High words of the bounds the hi-word compares use (checked against the
+// bisection thresholds in tests/test_capi_host.py::test_hiword_constants).
+constexpr int kHiHalfPi = 0x3ff921fb;    // pi/2 = quad[0]
+constexpr int kHiPiQ = 0x400921fb;       // pi = quad[1]
+constexpr int kHiThreeHalfPi = 0x4012d97c;  // RN(3pi/2) = quad[2]
+
 // Rows 0..5 are segments 0..5 (segments.hpp:33-66); the row is chosen by the
 // guess g = floor(red * 12/pi) (0..6 for red in [0, pi/2], 7 for NaN) and then
-// validated against its bracket.  Row 6 repeats segment 5 (red == pi/2 guesses
-// 6); row 7 never validates.  Row 0 starts at the smallest positive double,
-// not 0: a reduced angle of exactly +0 is sent to the exact path, which is what
-// makes dropping the r clamps sound (see fast_proposed).
+// validated against its bracket.  Row 0 accepts only hi(red) > 0 (red >= 2^-1022:
+// +0, -0 and negative red go to the exact path); row 5 stops below the high
+// word of pi/2 (red < pi/2 - 3.1e-7); rows 6 and 7 accept nothing.  Lanes
+// outside the brackets take the exact path (fast_proposed).  Tan-only kernels
+// use exact compares and the double bracket [klo, khi) instead: row 0 from the
+// smallest positive double, rows 5 and 6 up to +inf (red == pi/2 guesses 6),
+// row 7 (NaN) empty.
 struct SmemTable {
   SegRow row[8];
 };
 
 __device__ __forceinline__ void stage_table(SmemTable* s) {
-  const double inf = __longlong_as_double(0x7ff0000000000000ll);
   for (int i = threadIdx.x; i < 8; i += blockDim.x) {
     const int k = i < 6 ? i : 5;
     const Coeffs& c = c_table.seg[k];
-    const double klo = i == 0 ? __longlong_as_double(1) : i == 7 ? inf : c_table.knots[k];
-    const double khi = i >= 5 ? inf : c_table.knots[k + 1];
-    s->row[i] = SegRow{c.a, c.b, c.c, c.d, c.X, c.Y, c.Z, klo, khi, k, 0};
+    const int klo = i == 0 ? 0 : i >= 6 ? 0 : __double2hiint(c_table.knots[k]);
+    const int khi = i == 5 ? kHiHalfPi : i >= 6 ? 0 : __double2hiint(c_table.knots[k + 1]);
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    const double dlo = i == 0 ? __longlong_as_double(1) : i == 7 ? inf : c_table.knots[k];
+    const double dhi = i >= 5 ? inf : c_table.knots[k + 1];
+    s->row[i] = SegRow{c.a, c.b, c.c, c.d, c.X, c.Y, c.Z, klo, khi, dlo, dhi};
   }
 }
 
@@ -344,25 +365,37 @@ __device__ __forceinline__ double xor_hi(double v, unsigned bits) {
 
 // v^(-1/2) for the evaluation domain (radicand in [1.98e5, 8.9e5]; tan
 // denominator > 0.63 outside the pole window -- the only lanes whose tan value
-// is kept).  fisr.hpp:31-46 without the NaN guard, which cannot fire there;
-// 0.5*v as an exponent decrement (exact for these normal v).
+// is kept).  fisr.hpp:31-46 without the NaN guard, which cannot fire there.
+// The Newton step y*(1.5 - (0.5v*y)*y) is evaluated as y*fma(-0.5, (v*y)*y, 1.5):
+// 0.5v is exact, so RN(0.5v*y) = RN(v*y)/2 and RN(RN(0.5v*y)*y) = RN(RN(v*y)*y)/2
+// (no subnormals here), and the FMA of the exact product -0.5t with 1.5 rounds
+// once, as the reference's subtraction does -- same bits, no 0.5v to form.
+__device__ __forceinline__ double fisr_seed(double v) {
+  const unsigned hi = static_cast<unsigned>(__double2hiint(v));
+  const unsigned lo = static_cast<unsigned>(__double2loint(v));
+  // magic - (bits(v) >> 1) as one 64-bit subtract with borrow
+  unsigned ylo, yhi;
+  asm("sub.cc.u32 %0, %2, %3;\n\tsubc.u32 %1, %4, %5;"
+      : "=r"(ylo), "=r"(yhi)
+      : "r"(static_cast<unsigned>(kFisrMagic)), "r"(__funnelshift_r(lo, hi, 1)),
+        "r"(static_cast<unsigned>(kFisrMagic >> 32)), "r"(hi >> 1));
+  return __hiloint2double(static_cast<int>(yhi), static_cast<int>(ylo));
+}
+__device__ __forceinline__ double fisr_newton(double v, double y) {
+  return __dmul_rn(y, __fma_rn(-c_fast.half, __dmul_rn(__dmul_rn(v, y), y), 1.5));
+}
+
 template <int SQ>
 __device__ __forceinline__ double fast_rsqrt(double v, int steps) {
   if constexpr (SQ == kExact) {
     return __ddiv_rn(1.0, __dsqrt_rn(v));
   } else {
-    const unsigned hi = static_cast<unsigned>(__double2hiint(v));
-    const unsigned lo = static_cast<unsigned>(__double2loint(v));
-    const unsigned long long sh = (static_cast<unsigned long long>(hi >> 1) << 32) |
-                                  static_cast<unsigned long long>(__funnelshift_r(lo, hi, 1));
-    double y = u2d(kFisrMagic - sh);
-    const double half_v = __hiloint2double(static_cast<int>(hi - 0x00100000u), static_cast<int>(lo));
+    double y = fisr_seed(v);
     if constexpr (SQ == kFisr1 || SQ == kFisr2) {
-      y = __dmul_rn(y, __dsub_rn(1.5, __dmul_rn(__dmul_rn(half_v, y), y)));
-      if constexpr (SQ == kFisr2) y = __dmul_rn(y, __dsub_rn(1.5, __dmul_rn(__dmul_rn(half_v, y), y)));
+      y = fisr_newton(v, y);
+      if constexpr (SQ == kFisr2) y = fisr_newton(v, y);
     } else {
-      for (int i = 0; i < steps; ++i)
-        y = __dmul_rn(y, __dsub_rn(1.5, __dmul_rn(__dmul_rn(half_v, y), y)));
+      for (int i = 0; i < steps; ++i) y = fisr_newton(v, y);
     }
     return y;
   }
@@ -382,7 +415,7 @@ constexpr unsigned kLoPi = 0x54442d18u;  // pi, -pi, 2pi share the low word
 
 // CLAMP: apply the reference's r clamps (NaN-preserving form).  The proposed
 // path runs without them and validates instead (fast_proposed).
-template <bool NEED_SC, bool NEED_T, bool CLAMP>
+template <bool NEED_SC, bool NEED_T, bool CLAMP, bool HIW_T = !CLAMP>
 __device__ __forceinline__ FastRed fast_reduce(double x) {
   const FastConsts& K = c_fast;
   FastRed o{};
@@ -401,7 +434,18 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
     double r = __dsub_rn(a, __dmul_rn(K.two_pi, floor(q1)));
     if constexpr (CLAMP) r = (r < 0.0 || r >= K.two_pi) ? 0.0 : r;
     // reduction.hpp:44-52: q = floor(RN(r/(pi/2))) = p1 + p2 + p3
-    const bool p1 = r >= K.quad[0], p2 = r >= K.quad[1], p3 = r >= K.quad[2];
+    bool p1, p2, p3;
+    if constexpr (CLAMP) {
+      p1 = r >= K.quad[0], p2 = r >= K.quad[1], p3 = r >= K.quad[2];
+    } else {
+      // High words only, on the integer pipe: exact unless hi(r) equals a
+      // threshold's high word; such an r is given the lower quadrant, and if
+      // that is wrong its red lands within 2e-6 of 0 (r ~ pi) or of pi/2
+      // (r ~ pi/2, 3pi/2) -- never inside a row bracket (SmemTable), so the
+      // element takes the exact path.  r < 0 folds to red < 0 and NaN stays NaN.
+      const int rh = __double2hiint(r);
+      p1 = rh > kHiHalfPi, p2 = rh > kHiPiQ, p3 = rh > kHiThreeHalfPi;
+    }
     const bool odd = p1 ^ p2 ^ p3;
     const unsigned bhi = p3 ? kHiTwoPi : (p2 ? kHiMinusPi : (p1 ? kHiPi : 0u));
     const unsigned blo = p1 ? kLoPi : 0u;
@@ -412,9 +456,17 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
   }
   if constexpr (NEED_T) {
     // RN(a/pi) == 2*RN(a/2pi) exactly (2pi is an exact doubling of pi)
-    double r = __dsub_rn(a, __dmul_rn(K.pi, floor(__dadd_rn(q1, q1))));
+    // Proposed path: 2*q1 as an exponent increment (integer pipe).  Exact for
+    // normal q1; for q1 = 0 or subnormal both forms floor to 0.  Non-finite x
+    // (q1 NaN) gives r = +inf or NaN, whose fold fails every bracket; the
+    // Taylor path (CLAMP, no exact fallback) keeps the DADD so NaN survives.
+    const double q2 = CLAMP ? __dadd_rn(q1, q1)
+                            : __hiloint2double(__double2hiint(q1) + 0x00100000, __double2loint(q1));
+    double r = __dsub_rn(a, __dmul_rn(K.pi, floor(q2)));
     if constexpr (CLAMP) r = (r < 0.0 || r >= K.pi) ? 0.0 : r;
-    const bool up = r > K.half_pi;  // reduction.hpp:88-89
+    // reduction.hpp:88-89 (r > pi/2).  Proposed path: high word only; an r
+    // with the high word of pi/2 keeps red = r, whose high word no row accepts.
+    const bool up = HIW_T ? __double2hiint(r) > kHiHalfPi : r > K.half_pi;
     o.redt = __dadd_rn(__hiloint2double(up ? static_cast<int>(kHiPi) : 0, up ? static_cast<int>(kLoPi) : 0),
                        xor_hi(r, up ? 0x80000000u : 0u));
     o.neg_t = (up ? 0x80000000u : 0u) ^ xs;
@@ -443,10 +495,10 @@ static __device__ __noinline__ Out3 slow_proposed(double x, int method, int step
 // produce both segment choices even for functions not in MASK.
 //
 // Row choice: g = floor(red * 12/pi) from one fma.rz, validated by
-// klo <= red < khi (and the same for the tan angle, which differs from the
-// sin/cos one by a few ulps at most, so it shares the row).  A lane fails the
-// check only near a knot, at red == +0, for the r < 0 / r >= period cases the
-// reference clamps, or for non-finite x -- it then recomputes the element with
+// klo_hi < hi(red) < khi_hi (and the same for the tan angle, which differs from
+// the sin/cos one by a few ulps at most, so it shares the row).  A lane fails the
+// check only near a knot, at red == +0, within ~2e-6 of a quadrant boundary,
+// for the r < 0 / r >= period cases the reference clamps, or for non-finite x -- it then recomputes the element with
 // the exact device restatement (mirror_*), so every lane returns the
 // reference's bits.
 template <int SQ, unsigned MASK, bool SEG = false>
@@ -454,17 +506,32 @@ __device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, int
   constexpr bool kSC = (MASK & (kSin | kCos)) != 0 || SEG;
   constexpr bool kT = (MASK & kTan) != 0 || SEG;
   const FastConsts& K = c_fast;
-  const FastRed fr = fast_reduce<kSC, kT, false>(x);
+  // Tan-only kernels fold with the exact DSETP and validate with the exact
+  // bracket [klo, khi): measured faster there (444 vs 414 Gelem/s, cfg3) --
+  // the high-word bracket's extra LDS sits on that short kernel's critical path.
+  constexpr bool kDbl = !kSC;
+  const FastRed fr = fast_reduce<kSC, kT, false, !kDbl>(x);
   const double key = kSC ? fr.red : fr.redt;
   const unsigned g = static_cast<unsigned>(__double2loint(__fma_rz(key, K.twelve_over_pi, K.two52))) & 7u;
   const SegRow& s = tb.row[g];
+  // Z and the high-word bracket share one 16-byte chunk: one LDS.128
+  const int4 zq = *reinterpret_cast<const int4*>(&s.Z);
+  const double sZ = __hiloint2double(zq.y, zq.x);
   bool ok = true;
-  if constexpr (kSC) ok = fr.red >= s.klo && fr.red < s.khi;
-  if constexpr (kT) ok = ok && fr.redt >= s.klo && fr.redt < s.khi;
+  if constexpr (kSC) {
+    const int h = __double2hiint(fr.red);
+    ok = h > zq.z && h < zq.w;
+  }
+  if constexpr (kT && kDbl) {
+    ok = fr.redt >= s.klo && fr.redt < s.khi;
+  } else if constexpr (kT) {
+    const int h = __double2hiint(fr.redt);
+    ok = ok && h > zq.z && h < zq.w;
+  }
   Out3 o{0.0, 0.0, 0.0, 0, 0};
   if constexpr (kSC) {
     const double red = fr.red;
-    const double rad = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(s.X, red), s.Y), red), s.Z);
+    const double rad = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(s.X, red), s.Y), red), sZ);
     const double rs = fast_rsqrt<SQ>(rad, steps);
     if constexpr ((MASK & kSin) != 0)
       o.s = xor_hi(__dmul_rn(__dadd_rn(__dmul_rn(s.a, red), s.b), rs), fr.neg_s);
@@ -485,9 +552,9 @@ __device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, int
     v = fr.guard ? __longlong_as_double(0x7ff0000000000000ll) : v;
     o.t = xor_hi(v, fr.neg_t);
   }
-  if constexpr (SEG) {
-    o.seg_sc = s.seg;
-    o.seg_t = fr.guard ? 255 : s.seg;
+  if constexpr (SEG) {  // an accepted row is segment g (rows 0..5)
+    o.seg_sc = static_cast<int>(g);
+    o.seg_t = fr.guard ? 255 : static_cast<int>(g);
   }
   if (!ok) o = slow_proposed(x, SQ == kExact ? 0 : 1, SQ == kFisr1 ? 1 : SQ == kFisr2 ? 2 : steps);  // rare
   return o;

@@ -67,6 +67,28 @@ def test_thresholds_are_exact(ft):
     assert abs(g - hp) < 1e-3 and not abs(np.nextafter(g, 0.0) - hp) < 1e-3
 
 
+def test_hiword_constants(ft):
+    """The high-word compares of the fast path (ft_core.cuh kHi*) use the high
+    words of the bisection thresholds, and the zone argument holds: an r that
+    shares a threshold's high word but is given the lower quadrant folds to a
+    red whose high word no row bracket accepts (within 2e-6 of 0 or pi/2)."""
+    src = open(os.path.join(ROOT, "paper_2502_10831_b200", "csrc", "ft_core.cuh")).read()
+    const = {k: int(v, 16) for k, v in re.findall(r"constexpr int (kHi\w+) = (0x[0-9a-f]+);", src)}
+    th = ft.thresholds()
+    hi = lambda v: int(np.float64(v).view(np.uint64) >> np.uint64(32))  # noqa: E731
+    assert const == {"kHiHalfPi": hi(th[0]), "kHiPiQ": hi(th[1]), "kHiThreeHalfPi": hi(th[2])}
+    assert hi(th[0]) == hi(0.5 * math.pi)  # tan fold threshold (r > pi/2) shares it
+    P = math.pi
+    for k, t in enumerate(th[:3]):
+        top = (np.uint64(hi(t)) << np.uint64(32)) | np.uint64(0xFFFFFFFF)
+        r = np.array([t, top.view(np.float64)])  # the wrongly-folded part of the bucket
+        red = [r, P - r, r - P][k]  # lower-quadrant fold (reduction.hpp:59-79)
+        if k == 1:
+            assert (red <= 0).all()  # -> fails row 0 (hi(red) > 0)
+        else:
+            assert all(hi(v) >= const["kHiHalfPi"] for v in red)  # -> fails row 5's khi
+
+
 def test_invalid_arguments_fail_without_gpu(ft):
     from paper_2502_10831_b200 import _lib
 

@@ -108,6 +108,41 @@ def test_k1_adversarial_quotients(ft):
         check_against(xf, out, O.proposed(xf, 7, m, s, seg=True))
 
 
+def test_k1_hiword_zones(ft):
+    """The fast path compares high words only (quadrant, tan fold, row bracket,
+    ft_core.cuh fast_reduce/SmemTable): inputs whose r or red shares its high
+    word with pi/2, pi, RN(3pi/2) or a knot must still return the reference's
+    bits (they are assigned a conservative choice and redone exactly)."""
+    rng = np.random.default_rng(11)
+    xs = []
+    # r itself in each threshold's high-word bucket (x = r, period 0)
+    for hi in (0x3FF921FB, 0x400921FB, 0x4012D97C):
+        lo = np.concatenate([rng.integers(0, 1 << 32, 60000, dtype=np.uint64),
+                             np.arange(0, 64, dtype=np.uint64), (1 << 32) - 1 - np.arange(64, dtype=np.uint64)])
+        xs.append(((np.uint64(hi) << np.uint64(32)) | lo).view(np.float64))
+    # centres m*pi/12 (every knot and quadrant boundary of ~40 periods) +- a few
+    # high-word buckets
+    m = np.arange(0, 24 * 40)
+    c = np.repeat(m * (math.pi / 12), 2000)
+    xs.append(c + rng.uniform(-4e-6, 4e-6, c.size) * np.maximum(1.0, c / 8))
+    x = np.concatenate(xs)
+    x = np.concatenate([x, -x])
+    for m_, s in ((1, 1), (1, 2), (0, 0)):
+        out = ft.proposed_eval(dev(x), 7, ft.SqrtMode(m_, s), seg=True)
+        torch.cuda.synchronize()
+        check_against(x, out, O.proposed(x, 7, m_, s, seg=True))
+        for mask in (3, 4):  # sin/cos-only and tan-only kernels reduce once
+            out = ft.proposed_eval(dev(x), mask, ft.SqrtMode(m_, s))
+            torch.cuda.synchronize()
+            ref = O.proposed(x, mask, m_, s)
+            for f in out:
+                assert same_bits(host(out[f]), ref[f]), (mask, f)
+        xf = x.astype(np.float32)
+        out = ft.proposed_eval(dev(xf), 7, ft.SqrtMode(m_, s), seg=True)
+        torch.cuda.synchronize()
+        check_against(xf, out, O.proposed(xf, 7, m_, s, seg=True))
+
+
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 def test_device_generator_matches_host(ft, dtype):
     for w in (CONFIGS["cfg1"], CONFIGS["cfg2"], CONFIGS["cfg5"], PAPER_PROTOCOL):
