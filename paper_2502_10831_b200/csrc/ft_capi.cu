@@ -238,6 +238,10 @@ void parallel_copies(const std::vector<Copy>& copies) {
   for (auto& t : th) t.join();
 }
 
+template <class Launch>
+int host_pipeline_locked(HostPipe& p, int dev, std::size_t es, std::size_t chunk, const void* x,
+                         std::size_t n, unsigned mask, void* const out[3], Launch&& launch);
+
 // Chunked H2D -> kernel -> D2H over kPipe streams.  `launch(args, stream)`.
 template <class Launch>
 int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* const out[3],
@@ -252,6 +256,23 @@ int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* 
   std::lock_guard<std::mutex> lk(p.mu);
   int rc = pipe_reserve(p, std::max(chunk, kStageChunk) * es);  // device slots serve both paths
   if (rc) return rc;
+  rc = host_pipeline_locked(p, dev, es, chunk, x, n, mask, out, launch);
+  if (rc) {
+    // An early error return may leave chunks in flight on the pipeline streams;
+    // drain them so the next call cannot reuse slots that are still being read
+    // or written (the error string of the first failure is kept).
+    const std::string keep = g_err;
+    for (auto& s : p.st) (void)cudaStreamSynchronize(s);
+    (void)cudaGetLastError();
+    g_err = keep;
+  }
+  return rc;
+}
+
+template <class Launch>
+int host_pipeline_locked(HostPipe& p, int dev, std::size_t es, std::size_t chunk, const void* x,
+                         std::size_t n, unsigned mask, void* const out[3], Launch&& launch) {
+  int rc = FT_OK;
   const char* xb = static_cast<const char*>(x);
   const bool x_pinned = host_pinned(x);
   bool o_pinned = true;

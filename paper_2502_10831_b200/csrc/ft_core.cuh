@@ -502,7 +502,7 @@ static __device__ __noinline__ Out3 slow_proposed(double x, int method, int step
 // the exact device restatement (mirror_*), so every lane returns the
 // reference's bits.
 template <int SQ, unsigned MASK, bool SEG = false>
-__device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, int steps) {
+__device__ __forceinline__ Out3 fast_proposed_core(double x, const SmemTable& tb, int steps, bool* okp) {
   constexpr bool kSC = (MASK & (kSin | kCos)) != 0 || SEG;
   constexpr bool kT = (MASK & kTan) != 0 || SEG;
   const FastConsts& K = c_fast;
@@ -556,7 +556,20 @@ __device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, int
     o.seg_sc = static_cast<int>(g);
     o.seg_t = fr.guard ? 255 : static_cast<int>(g);
   }
-  if (!ok) o = slow_proposed(x, SQ == kExact ? 0 : 1, SQ == kFisr1 ? 1 : SQ == kFisr2 ? 2 : steps);  // rare
+  *okp = ok;
+  return o;
+}
+
+template <int SQ>
+__device__ __forceinline__ Out3 slow_proposed_mode(double x, int steps) {
+  return slow_proposed(x, SQ == kExact ? 0 : 1, SQ == kFisr1 ? 1 : SQ == kFisr2 ? 2 : steps);
+}
+
+template <int SQ, unsigned MASK, bool SEG = false>
+__device__ __forceinline__ Out3 fast_proposed(double x, const SmemTable& tb, int steps) {
+  bool ok;
+  Out3 o = fast_proposed_core<SQ, MASK, SEG>(x, tb, steps, &ok);
+  if (!ok) o = slow_proposed_mode<SQ>(x, steps);  // rare
   return o;
 }
 

@@ -27,8 +27,17 @@ template <typename T>
 constexpr bool kTmaK1 = sizeof(T) == 8 && FT_TMA_F64;
 template <typename T>
 constexpr bool kTmaK2 = (sizeof(T) == 8 && FT_TMA_F64) || (sizeof(T) == 4 && FT_TMA_TAYLOR_F32);
+#ifndef FT_MINB_F32
+#define FT_MINB_F32 4  // resident blocks/SM the f32 kernels are compiled for (register cap)
+#endif
 template <typename T>
-constexpr int kMinBlocks = kTmaK1<T> ? 3 : 4;
+constexpr int kMinBlocks = kTmaK1<T> ? 3 : FT_MINB_F32;
+// Where the exact-path branch sits: 0 one per element; 1 one per vector for
+// tan-only kernels (cfg3 +5%; the fused kernels lose 10% to the extra live
+// registers at the 64-register cap); 2 one per vector everywhere.
+#ifndef FT_BATCH_SLOW
+#define FT_BATCH_SLOW 1
+#endif
 #ifndef FT_RPF
 #define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
 #endif
@@ -97,14 +106,35 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
       T xs[VN], rs[VN], rc[VN], rt[VN];
       std::uint8_t g0[VN], g1[VN];
       V::unpack(xin, xs);
-#pragma unroll
-      for (int j = 0; j < VN; ++j) {
-        const Out3 o = op(static_cast<double>(xs[j]));
+      auto put = [&](int j, const Out3& o) {
         rs[j] = to_out<T>(o.s);
         rc[j] = to_out<T>(o.c);
         rt[j] = to_out<T>(o.t);
         g0[j] = static_cast<std::uint8_t>(o.seg_sc);
         g1[j] = static_cast<std::uint8_t>(o.seg_t);
+      };
+      if constexpr (Op::kBatched) {
+        // Fast path for every element first (no branch between them, so the
+        // compiler can interleave the elements' dependency chains), then one
+        // rarely-taken branch that redoes the failing ones exactly.
+        Out3 ov[VN];
+        bool okv[VN];
+        bool all = true;
+#pragma unroll
+        for (int j = 0; j < VN; ++j) {
+          ov[j] = op.core(static_cast<double>(xs[j]), &okv[j]);
+          all = all && okv[j];
+        }
+        if (!all) {
+#pragma unroll
+          for (int j = 0; j < VN; ++j)
+            if (!okv[j]) ov[j] = op.slow(static_cast<double>(xs[j]));
+        }
+#pragma unroll
+        for (int j = 0; j < VN; ++j) put(j, ov[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < VN; ++j) put(j, op(static_cast<double>(xs[j])));
       }
       res[0] = V::pack(rs);
       res[1] = V::pack(rc);
@@ -198,15 +228,21 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
 
 template <int SQ, unsigned MASK, bool SEG>
 struct ProposedOp {
+  static constexpr bool kBatched = FT_BATCH_SLOW == 2 || (FT_BATCH_SLOW == 1 && MASK == kTan);
   const SmemTable* tb;
   int steps;
   __device__ __forceinline__ Out3 operator()(double x) const {
     return fast_proposed<SQ, MASK, SEG>(x, *tb, steps);
   }
+  __device__ __forceinline__ Out3 core(double x, bool* ok) const {
+    return fast_proposed_core<SQ, MASK, SEG>(x, *tb, steps, ok);
+  }
+  __device__ __forceinline__ Out3 slow(double x) const { return slow_proposed_mode<SQ>(x, steps); }
 };
 
 template <int NT, unsigned MASK>
 struct TaylorOp {
+  static constexpr bool kBatched = false;
   int n;
   __device__ __forceinline__ Out3 operator()(double x) const { return fast_taylor<NT, MASK>(x, n); }
 };
@@ -215,6 +251,7 @@ struct TaylorOp {
 // reference scalar code does (kernels.hpp:46-67 / SPEC.md:224-247).
 template <unsigned MASK>
 struct MirrorOp {
+  static constexpr bool kBatched = false;
   int kind, method, steps, n;
   __device__ __forceinline__ Out3 operator()(double x) const {
     Out3 o{0.0, 0.0, 0.0, 0, 0};
