@@ -314,15 +314,17 @@ static_assert(kRowBytes == 80, "row stride");
 constexpr int kHiHalfPi = 0x3ff921fb;    // pi/2 = quad[0]
 constexpr int kHiPiQ = 0x400921fb;       // pi = quad[1]
 constexpr int kHiThreeHalfPi = 0x4012d97c;  // RN(3pi/2) = quad[2]
+constexpr int kHiRow0Lo = 0x3ee00000;       // 2^-17: row 0 accepts hi(red) > this
 
 // Rows 0..5 are segments 0..5 (segments.hpp:33-66); the row is chosen by the
 // guess g = floor(red * 12/pi) (0..6 for red in [0, pi/2], 7 for NaN) and then
-// validated against its bracket.  Row 0 accepts only hi(red) > 0 (red >= 2^-1022:
-// +0, -0 and negative red go to the exact path); row 5 stops below the high
+// validated against its bracket.  Row 0 accepts only hi(red) > hi(2^-17) (red
+// >= 2^-17 + 2^-37: +0, tiny and negative red go to the exact path, which also
+// covers the quadrant mis-folds of fast_reduce); row 5 stops below the high
 // word of pi/2 (red < pi/2 - 3.1e-7); rows 6 and 7 accept nothing.  Lanes
 // outside the brackets take the exact path (fast_proposed).  Tan-only kernels
-// use exact compares and the double bracket [klo, khi) instead: row 0 from the
-// smallest positive double, rows 5 and 6 up to +inf (red == pi/2 guesses 6),
+// use exact compares and the double bracket [klo, khi) instead: row 0 from
+// 2^-17, rows 5 and 6 up to +inf (red == pi/2 guesses 6),
 // row 7 (NaN) empty.
 struct SmemTable {
   SegRow row[8];
@@ -332,10 +334,10 @@ __device__ __forceinline__ void stage_table(SmemTable* s) {
   for (int i = threadIdx.x; i < 8; i += blockDim.x) {
     const int k = i < 6 ? i : 5;
     const Coeffs& c = c_table.seg[k];
-    const int klo = i == 0 ? 0 : i >= 6 ? 0 : __double2hiint(c_table.knots[k]);
+    const int klo = i == 0 ? kHiRow0Lo : i >= 6 ? 0 : __double2hiint(c_table.knots[k]);
     const int khi = i == 5 ? kHiHalfPi : i >= 6 ? 0 : __double2hiint(c_table.knots[k + 1]);
     const double inf = __longlong_as_double(0x7ff0000000000000ll);
-    const double dlo = i == 0 ? __longlong_as_double(1) : i == 7 ? inf : c_table.knots[k];
+    const double dlo = i == 0 ? 0x1p-17 : i == 7 ? inf : c_table.knots[k];
     const double dhi = i >= 5 ? inf : c_table.knots[k + 1];
     s->row[i] = SegRow{c.a, c.b, c.c, c.d, c.X, c.Y, c.Z, klo, khi, dlo, dhi};
   }
@@ -370,16 +372,13 @@ __device__ __forceinline__ double xor_hi(double v, unsigned bits) {
 // 0.5v is exact, so RN(0.5v*y) = RN(v*y)/2 and RN(RN(0.5v*y)*y) = RN(RN(v*y)*y)/2
 // (no subnormals here), and the FMA of the exact product -0.5t with 1.5 rounds
 // once, as the reference's subtraction does -- same bits, no 0.5v to form.
+// magic - (bits >> 1) == (2*magic + 1 - bits) >> 1 for bits <= 2*magic + 1 (all
+// positive doubles): with bits = 2k + e, floor((2m + 1 - 2k - e) / 2) = m - k.
+// One 64-bit subtract then one 64-bit shift (4 integer instructions, vs 5 for
+// shift-then-subtract, whose subtrahend needs a complement).
+constexpr std::uint64_t kFisrMagic2p1 = 2 * kFisrMagic + 1;
 __device__ __forceinline__ double fisr_seed(double v) {
-  const unsigned hi = static_cast<unsigned>(__double2hiint(v));
-  const unsigned lo = static_cast<unsigned>(__double2loint(v));
-  // magic - (bits(v) >> 1) as one 64-bit subtract with borrow
-  unsigned ylo, yhi;
-  asm("sub.cc.u32 %0, %2, %3;\n\tsubc.u32 %1, %4, %5;"
-      : "=r"(ylo), "=r"(yhi)
-      : "r"(static_cast<unsigned>(kFisrMagic)), "r"(__funnelshift_r(lo, hi, 1)),
-        "r"(static_cast<unsigned>(kFisrMagic >> 32)), "r"(hi >> 1));
-  return __hiloint2double(static_cast<int>(yhi), static_cast<int>(ylo));
+  return u2d((kFisrMagic2p1 - d2u(v)) >> 1);
 }
 __device__ __forceinline__ double fisr_newton(double v, double y) {
   return __dmul_rn(y, __fma_rn(-c_fast.half, __dmul_rn(__dmul_rn(v, y), y), 1.5));
@@ -408,6 +407,7 @@ struct FastRed {
   unsigned neg_c;
   unsigned neg_t;
   bool guard;      // tan pole window (kernels.hpp:62)
+  bool valid;      // proposed path: r within [0, 2pi]'s high words (see fast_reduce)
 };
 
 constexpr unsigned kHiPi = 0x400921fbu, kHiTwoPi = 0x401921fbu, kHiMinusPi = 0xc00921fbu;
@@ -419,13 +419,28 @@ template <bool NEED_SC, bool NEED_T, bool CLAMP, bool HIW_T = !CLAMP>
 __device__ __forceinline__ FastRed fast_reduce(double x) {
   const FastConsts& K = c_fast;
   FastRed o{};
+  o.valid = true;
   const double a = fabs(x);
   // q1 = RN(a / 2pi) exactly: y = RN(1/2pi) is within 0.206*2^-53 relative, so
   // q0 = RN(a*y) is within 0.912 ulp of a/2pi and one Markstein correction
   // (exact FMA remainder) rounds to RN(a/2pi).
   const double q0 = __dmul_rn(a, K.inv_two_pi);
-  const double rem = __fma_rn(-q0, K.two_pi, a);
-  const double q1 = __fma_rn(rem, K.inv_two_pi, q0);
+  double q1 = q0;
+  if constexpr (CLAMP) {
+    const double rem = __fma_rn(-q0, K.two_pi, a);
+    q1 = __fma_rn(rem, K.inv_two_pi, q0);
+  } else {
+    // Proposed path: no correction.  q0 differs from RN(a/2pi) by at most one
+    // ulp, so floor(q0) differs from the reference's floor only when an
+    // integer k lies between them, i.e. a is within ~a*2^-52 of 2pi*k (or pi*k
+    // for tan).  The r that follows is then off by one period: r <= 0 (+0
+    // when a == RN(2pi*k)), or r within that distance of 2pi (pi), whose fold
+    // is <= 0 or smaller than 2^-22 for |x| < 2^30 -- no row bracket accepts
+    // either, so those elements take the exact path
+    // (tests/test_capi_host.py::test_markstein_free_floor_is_caught).  |x| >= 2^30 always does (`valid`:
+    // q0 < 2^27, i.e. |x| < 2^27 * 2pi < 2^30; NaN and inf fail it too).
+    o.valid = __double2hiint(q0) < 0x41a00000;
+  }
   const unsigned xs = static_cast<unsigned>(__double2hiint(x)) & 0x80000000u;
   if constexpr (NEED_SC) {
     // reduction.hpp:26-30 (period 2pi) without its two clamps: r < 0 or
@@ -437,20 +452,30 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
     bool p1, p2, p3;
     if constexpr (CLAMP) {
       p1 = r >= K.quad[0], p2 = r >= K.quad[1], p3 = r >= K.quad[2];
+      const bool odd = p1 ^ p2 ^ p3;
+      const unsigned bhi = p3 ? kHiTwoPi : (p2 ? kHiMinusPi : (p1 ? kHiPi : 0u));
+      const unsigned blo = p1 ? kLoPi : 0u;
+      o.red = __dadd_rn(__hiloint2double(static_cast<int>(bhi), static_cast<int>(blo)),
+                        xor_hi(r, odd ? 0x80000000u : 0u));
     } else {
       // High words only, on the integer pipe: exact unless hi(r) equals a
-      // threshold's high word; such an r is given the lower quadrant, and if
-      // that is wrong its red lands within 2e-6 of 0 (r ~ pi) or of pi/2
-      // (r ~ pi/2, 3pi/2) -- never inside a row bracket (SmemTable), so the
-      // element takes the exact path.  r < 0 folds to red < 0 and NaN stays NaN.
+      // threshold's high word; such an r may be given the lower quadrant.
       const int rh = __double2hiint(r);
       p1 = rh > kHiHalfPi, p2 = rh > kHiPiQ, p3 = rh > kHiThreeHalfPi;
+      // Fold as red = |RN(r - c)|, c = 0, pi, pi, 2pi for q = 0..3: RN is odd,
+      // so RN(pi - r) = -RN(r - pi) and RN(2pi - r) = -RN(r - 2pi).  A wrong
+      // quadrant from the high-word compares puts red within 2^-19 of 0
+      // (r ~ pi: same |red|, wrong sine sign) or at/above pi/2 (r ~ pi/2,
+      // 3pi/2); r < 0 and r beyond 2pi's high word (the reference's clamps,
+      // NaN) are caught by `valid`, r sharing 2pi's high word gives
+      // red < 2^-18.  No row bracket accepts red < 2^-17 or hi(red) >=
+      // hi(pi/2) (SmemTable), so all of these take the exact path.
+      const unsigned chi = p3 ? kHiTwoPi : (p1 ? kHiPi : 0u);
+      const unsigned clo = p1 ? kLoPi : 0u;
+      const double d = __dsub_rn(r, __hiloint2double(static_cast<int>(chi), static_cast<int>(clo)));
+      o.red = __hiloint2double(__double2hiint(d) & 0x7fffffff, __double2loint(d));  // |d|, integer pipe
+      o.valid = o.valid & (static_cast<unsigned>(rh) <= kHiTwoPi);
     }
-    const bool odd = p1 ^ p2 ^ p3;
-    const unsigned bhi = p3 ? kHiTwoPi : (p2 ? kHiMinusPi : (p1 ? kHiPi : 0u));
-    const unsigned blo = p1 ? kLoPi : 0u;
-    o.red = __dadd_rn(__hiloint2double(static_cast<int>(bhi), static_cast<int>(blo)),
-                      xor_hi(r, odd ? 0x80000000u : 0u));
     o.neg_s = (p2 ? 0x80000000u : 0u) ^ xs;  // q >= 2, odd symmetry (reduction.hpp:65-66)
     o.neg_c = (p1 != p3) ? 0x80000000u : 0u; // q in {1, 2} (reduction.hpp:77)
   }
@@ -520,13 +545,13 @@ __device__ __forceinline__ Out3 fast_proposed_core(double x, const SmemTable& tb
   bool ok = true;
   if constexpr (kSC) {
     const int h = __double2hiint(fr.red);
-    ok = h > zq.z && h < zq.w;
+    ok = fr.valid & (h > zq.z) & (h < zq.w);
   }
   if constexpr (kT && kDbl) {
-    ok = fr.redt >= s.klo && fr.redt < s.khi;
+    ok = fr.valid & (fr.redt >= s.klo) & (fr.redt < s.khi);
   } else if constexpr (kT) {
     const int h = __double2hiint(fr.redt);
-    ok = ok && h > zq.z && h < zq.w;
+    ok = ok & (h > zq.z) & (h < zq.w);
   }
   Out3 o{0.0, 0.0, 0.0, 0, 0};
   if constexpr (kSC) {

@@ -38,6 +38,9 @@ constexpr int kMinBlocks = kTmaK1<T> ? 3 : FT_MINB_F32;
 #ifndef FT_BATCH_SLOW
 #define FT_BATCH_SLOW 1
 #endif
+#ifndef FT_PAIR
+#define FT_PAIR 0  // 1: f32 fused kernels branch once per pair of elements
+#endif
 #ifndef FT_RPF
 #define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
 #endif
@@ -113,25 +116,30 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
         g0[j] = static_cast<std::uint8_t>(o.seg_sc);
         g1[j] = static_cast<std::uint8_t>(o.seg_t);
       };
-      if constexpr (Op::kBatched) {
-        // Fast path for every element first (no branch between them, so the
-        // compiler can interleave the elements' dependency chains), then one
-        // rarely-taken branch that redoes the failing ones exactly.
-        Out3 ov[VN];
-        bool okv[VN];
-        bool all = true;
+      constexpr int G = Op::template kGroup<T> < VN ? Op::template kGroup<T> : VN;
+      if constexpr (G > 1) {
+        // Groups of G elements: the fast path of every element of the group
+        // first (no branch between them, so the compiler can interleave their
+        // dependency chains), then one rarely-taken branch that redoes the
+        // failing ones exactly.
 #pragma unroll
-        for (int j = 0; j < VN; ++j) {
-          ov[j] = op.core(static_cast<double>(xs[j]), &okv[j]);
-          all = all && okv[j];
+        for (int j0 = 0; j0 < VN; j0 += G) {
+          Out3 ov[G];
+          bool okv[G];
+          bool all = true;
+#pragma unroll
+          for (int j = 0; j < G; ++j) {
+            ov[j] = op.core(static_cast<double>(xs[j0 + j]), &okv[j]);
+            all = all && okv[j];
+          }
+          if (!all) {
+#pragma unroll
+            for (int j = 0; j < G; ++j)
+              if (!okv[j]) ov[j] = op.slow(static_cast<double>(xs[j0 + j]));
+          }
+#pragma unroll
+          for (int j = 0; j < G; ++j) put(j0 + j, ov[j]);
         }
-        if (!all) {
-#pragma unroll
-          for (int j = 0; j < VN; ++j)
-            if (!okv[j]) ov[j] = op.slow(static_cast<double>(xs[j]));
-        }
-#pragma unroll
-        for (int j = 0; j < VN; ++j) put(j, ov[j]);
       } else {
 #pragma unroll
         for (int j = 0; j < VN; ++j) put(j, op(static_cast<double>(xs[j])));
@@ -228,7 +236,10 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
 
 template <int SQ, unsigned MASK, bool SEG>
 struct ProposedOp {
-  static constexpr bool kBatched = FT_BATCH_SLOW == 2 || (FT_BATCH_SLOW == 1 && MASK == kTan);
+  // Elements per exact-path branch (see stream_map).
+  template <typename T>
+  static constexpr int kGroup =
+      FT_BATCH_SLOW == 2 ? 4 : (FT_BATCH_SLOW == 1 && MASK == kTan) ? 4 : (FT_PAIR && sizeof(T) == 4) ? 2 : 1;
   const SmemTable* tb;
   int steps;
   __device__ __forceinline__ Out3 operator()(double x) const {
@@ -242,7 +253,8 @@ struct ProposedOp {
 
 template <int NT, unsigned MASK>
 struct TaylorOp {
-  static constexpr bool kBatched = false;
+  template <typename T>
+  static constexpr int kGroup = 1;
   int n;
   __device__ __forceinline__ Out3 operator()(double x) const { return fast_taylor<NT, MASK>(x, n); }
 };
@@ -251,7 +263,8 @@ struct TaylorOp {
 // reference scalar code does (kernels.hpp:46-67 / SPEC.md:224-247).
 template <unsigned MASK>
 struct MirrorOp {
-  static constexpr bool kBatched = false;
+  template <typename T>
+  static constexpr int kGroup = 1;
   int kind, method, steps, n;
   __device__ __forceinline__ Out3 operator()(double x) const {
     Out3 o{0.0, 0.0, 0.0, 0, 0};

@@ -70,23 +70,75 @@ def test_thresholds_are_exact(ft):
 def test_hiword_constants(ft):
     """The high-word compares of the fast path (ft_core.cuh kHi*) use the high
     words of the bisection thresholds, and the zone argument holds: an r that
-    shares a threshold's high word but is given the lower quadrant folds to a
-    red whose high word no row bracket accepts (within 2e-6 of 0 or pi/2)."""
+    shares a threshold's high word but is given the lower quadrant folds
+    (red = |r - c|, c = 0, pi, pi, 2pi) to a red that no row bracket accepts --
+    below row 0's lower bound 2^-17 (r ~ pi, r ~ 2pi) or with the high word of
+    pi/2 or above (r ~ pi/2, 3pi/2)."""
     src = open(os.path.join(ROOT, "paper_2502_10831_b200", "csrc", "ft_core.cuh")).read()
     const = {k: int(v, 16) for k, v in re.findall(r"constexpr int (kHi\w+) = (0x[0-9a-f]+);", src)}
     th = ft.thresholds()
     hi = lambda v: int(np.float64(v).view(np.uint64) >> np.uint64(32))  # noqa: E731
-    assert const == {"kHiHalfPi": hi(th[0]), "kHiPiQ": hi(th[1]), "kHiThreeHalfPi": hi(th[2])}
+    assert const == {"kHiHalfPi": hi(th[0]), "kHiPiQ": hi(th[1]), "kHiThreeHalfPi": hi(th[2]),
+                     "kHiRow0Lo": hi(2.0 ** -17)}
     assert hi(th[0]) == hi(0.5 * math.pi)  # tan fold threshold (r > pi/2) shares it
     P = math.pi
+    bottom = lambda t: (np.uint64(hi(t)) << np.uint64(32)).view(np.float64)  # noqa: E731
+    top = lambda t: ((np.uint64(hi(t)) << np.uint64(32)) | np.uint64(0xFFFFFFFF)).view(np.float64)  # noqa: E731
     for k, t in enumerate(th[:3]):
-        top = (np.uint64(hi(t)) << np.uint64(32)) | np.uint64(0xFFFFFFFF)
-        r = np.array([t, top.view(np.float64)])  # the wrongly-folded part of the bucket
-        red = [r, P - r, r - P][k]  # lower-quadrant fold (reduction.hpp:59-79)
+        r = np.array([t, top(t)])  # the wrongly-folded part of the bucket
+        red = np.abs([r, r - P, r - P][k])  # lower-quadrant fold
         if k == 1:
-            assert (red <= 0).all()  # -> fails row 0 (hi(red) > 0)
+            assert all(hi(v) <= const["kHiRow0Lo"] for v in red)  # -> fails row 0
         else:
             assert all(hi(v) >= const["kHiHalfPi"] for v in red)  # -> fails row 5's khi
+    # r sharing 2pi's high word passes `valid`, folds with c = 2pi: tiny red
+    r = np.array([bottom(2 * P), 2 * P, top(2 * P)])
+    assert all(hi(v) <= const["kHiRow0Lo"] for v in np.abs(r - 2 * P))
+
+
+def test_fisr_seed_identity():
+    """ft_core.cuh fisr_seed: magic - (b >> 1) == (2*magic + 1 - b) >> 1 for
+    every positive double bit pattern b (fisr.hpp:38-40)."""
+    M = 0x5FE6EB50C7B537A9
+    rng = np.random.default_rng(5)
+    bs = [int(v) for v in rng.integers(0, 0x7FF0000000000000, 200000, dtype=np.uint64)]
+    bs += [0, 1, 2, 0x7FEFFFFFFFFFFFFF, 0x7FF0000000000000, 0x3FF0000000000000, 0x3FF0000000000001]
+    for b in bs:
+        assert M - (b >> 1) == (2 * M + 1 - b) >> 1
+
+
+def test_markstein_free_floor_is_caught():
+    """ft_core.cuh fast_reduce (proposed path) floors q0 = RN(a * RN(1/2pi))
+    instead of RN(a/2pi).  Wherever the floors differ (a within ~a*2^-52 of a
+    multiple of 2pi or pi), the r it produces must be rejected downstream:
+    r < 2^-17, or r within 2^-17 of the period (folds below row 0's bound).
+    Checked on the adversarial neighbourhoods of k*2pi and k*pi for |x| < 2^30
+    (plus random a), in binary64 with the reference's operation order."""
+    P = math.pi
+    y = 1.0 / (2.0 * P)
+    rng = np.random.default_rng(11)
+    ks = np.unique(np.concatenate([np.arange(1, 5000), rng.integers(1, 2**27, 20000)])).astype(np.float64)
+    checked = 0
+    for period, scale in ((2.0 * P, 1.0), (P, 2.0)):
+        base = ks * period
+        a = base[:, None].copy()
+        # +-8 ulps around each multiple
+        offs = np.arange(-8, 9)
+        a = (base[:, None].view(np.int64) + offs[None, :]).view(np.float64).ravel()
+        a = a[(a > 0) & (a < 2.0**30)]
+        q0 = a * y
+        q1 = a / (2.0 * P)
+        f0 = np.floor(q0 * scale)  # tan: floor(2*q0) (exact doubling)
+        f1 = np.floor(q1 * scale)
+        diff = f0 != f1
+        r_ref = a[diff] - period * f1[diff]
+        r_ours = a[diff] - period * f0[diff]
+        # ours is off by one period: below 2^-17 (negative, or an exact 0 when
+        # a == RN(period*k)), or within 2^-17 of `period`
+        assert ((r_ours < 2.0**-17) | (np.abs(r_ours - period) < 2.0**-17)).all()
+        checked += int(diff.sum())
+        assert (np.abs(np.abs(r_ours - r_ref) - period) < 1e-6).all()
+    assert checked > 0  # the neighbourhoods do contain floor disagreements
 
 
 def test_invalid_arguments_fail_without_gpu(ft):
