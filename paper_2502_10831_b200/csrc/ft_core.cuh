@@ -39,6 +39,7 @@
 //             separately rounded.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -343,22 +344,13 @@ __device__ __forceinline__ void stage_table(SmemTable* s) {
   }
 }
 
-// Byte offset of the row for reduced angle `red` (segments.hpp:70-73: knot k
-// opens segment k).  NaN -> row 0.  (Exact search; the fast path uses the
-// bracket-validated guess instead.)
-__device__ __forceinline__ unsigned seg_off(double red) {
-  const FastConsts& K = c_fast;
-  unsigned off = 0;
-  off = red >= K.knot[0] ? 1 * kRowBytes : off;
-  off = red >= K.knot[1] ? 2 * kRowBytes : off;
-  off = red >= K.knot[2] ? 3 * kRowBytes : off;
-  off = red >= K.knot[3] ? 4 * kRowBytes : off;
-  off = red >= K.knot[4] ? 5 * kRowBytes : off;
-  return off;
+__device__ __forceinline__ void lds_f64x2(unsigned addr, double& a, double& b) {
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr));
 }
-
-__device__ __forceinline__ const SegRow& row_at(const SmemTable& tb, unsigned off) {
-  return *reinterpret_cast<const SegRow*>(reinterpret_cast<const char*>(&tb) + off);
+__device__ __forceinline__ int4 lds_i32x4(unsigned addr) {
+  int4 v;
+  asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ double xor_hi(double v, unsigned bits) {
@@ -442,11 +434,14 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
     o.valid = __double2hiint(q0) < 0x41a00000;
   }
   const unsigned xs = static_cast<unsigned>(__double2hiint(x)) & 0x80000000u;
+  double k = 0.0;       // floor(q1)
+  bool upper = false;   // proposed path: r >= pi by the high-word compare
   if constexpr (NEED_SC) {
-    // reduction.hpp:26-30 (period 2pi) without its two clamps: r < 0 or
-    // r >= 2pi folds to red <= 0 (or NaN), which fails the row bracket and
+    // reduction.hpp:26-30 (period 2pi) without its two clamps on the proposed
+    // path: r < 0 or r >= 2pi is caught by `valid` / the row brackets and
     // takes the exact path (fast_proposed).
-    double r = __dsub_rn(a, __dmul_rn(K.two_pi, floor(q1)));
+    k = floor(q1);
+    double r = __dsub_rn(a, __dmul_rn(K.two_pi, k));
     if constexpr (CLAMP) r = (r < 0.0 || r >= K.two_pi) ? 0.0 : r;
     // reduction.hpp:44-52: q = floor(RN(r/(pi/2))) = p1 + p2 + p3
     bool p1, p2, p3;
@@ -475,9 +470,13 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
       const double d = __dsub_rn(r, __hiloint2double(static_cast<int>(chi), static_cast<int>(clo)));
       o.red = __hiloint2double(__double2hiint(d) & 0x7fffffff, __double2loint(d));  // |d|, integer pipe
       o.valid = o.valid & (static_cast<unsigned>(rh) <= kHiTwoPi);
+      // cos sign: q in {1, 2} == (q >= 2) xor (q odd), and q is odd exactly
+      // when r - c < 0 (q = 1, 3), so it is the sign bit of d xor p2.
+      o.neg_c = (static_cast<unsigned>(__double2hiint(d)) & 0x80000000u) ^ (p2 ? 0x80000000u : 0u);
+      upper = p2;
     }
     o.neg_s = (p2 ? 0x80000000u : 0u) ^ xs;  // q >= 2, odd symmetry (reduction.hpp:65-66)
-    o.neg_c = (p1 != p3) ? 0x80000000u : 0u; // q in {1, 2} (reduction.hpp:77)
+    if constexpr (CLAMP) o.neg_c = (p1 != p3) ? 0x80000000u : 0u;  // q in {1, 2} (reduction.hpp:77)
   }
   if constexpr (NEED_T) {
     // RN(a/pi) == 2*RN(a/2pi) exactly (2pi is an exact doubling of pi)
@@ -485,9 +484,21 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
     // normal q1; for q1 = 0 or subnormal both forms floor to 0.  Non-finite x
     // (q1 NaN) gives r = +inf or NaN, whose fold fails every bracket; the
     // Taylor path (CLAMP, no exact fallback) keeps the DADD so NaN survives.
-    const double q2 = CLAMP ? __dadd_rn(q1, q1)
-                            : __hiloint2double(__double2hiint(q1) + 0x00100000, __double2loint(q1));
-    double r = __dsub_rn(a, __dmul_rn(K.pi, floor(q2)));
+    double r;
+    if constexpr (NEED_SC && !CLAMP) {
+      // Fused proposed path: floor(RN(a/pi)) = 2k + [r >= pi] for the sine's
+      // k and r, and RN(pi * (2k + s)) = fma(k, 2pi, s ? pi : 0) (2pi = 2 * pi
+      // exactly, so the FMA rounds the same real number once).  When the
+      // high-word `upper` is wrong (r within 2^-19 of pi) or k is off by one,
+      // the tangent's r is off by one period and folds to red_t <= 0 or below
+      // 2^-17 -- rejected like the sine's (see above).
+      const double s_pi = __hiloint2double(upper ? static_cast<int>(kHiPi) : 0, upper ? static_cast<int>(kLoPi) : 0);
+      r = __dsub_rn(a, __fma_rn(k, K.two_pi, s_pi));
+    } else {
+      const double q2 = CLAMP ? __dadd_rn(q1, q1)
+                              : __hiloint2double(__double2hiint(q1) + 0x00100000, __double2loint(q1));
+      r = __dsub_rn(a, __dmul_rn(K.pi, floor(q2)));
+    }
     if constexpr (CLAMP) r = (r < 0.0 || r >= K.pi) ? 0.0 : r;
     // reduction.hpp:88-89 (r > pi/2).  Proposed path: high word only; an r
     // with the high word of pi/2 keeps red = r, whose high word no row accepts.
@@ -538,9 +549,16 @@ __device__ __forceinline__ Out3 fast_proposed_core(double x, const SmemTable& tb
   const FastRed fr = fast_reduce<kSC, kT, false, !kDbl>(x);
   const double key = kSC ? fr.red : fr.redt;
   const unsigned g = static_cast<unsigned>(__double2loint(__fma_rz(key, K.twelve_over_pi, K.two52))) & 7u;
-  const SegRow& s = tb.row[g];
+  // Row loads as ld.shared from the table's 32-bit shared address (a generic
+  // pointer costs the loop a CTA-window base re-materialisation per element).
+  const unsigned ra = static_cast<unsigned>(__cvta_generic_to_shared(&tb)) + g * kRowBytes;
+  SegRow s;
+  lds_f64x2(ra + offsetof(SegRow, a), s.a, s.b);
+  lds_f64x2(ra + offsetof(SegRow, c), s.c, s.d);
+  lds_f64x2(ra + offsetof(SegRow, X), s.X, s.Y);
+  lds_f64x2(ra + offsetof(SegRow, klo), s.klo, s.khi);
   // Z and the high-word bracket share one 16-byte chunk: one LDS.128
-  const int4 zq = *reinterpret_cast<const int4*>(&s.Z);
+  const int4 zq = lds_i32x4(ra + offsetof(SegRow, Z));
   const double sZ = __hiloint2double(zq.y, zq.x);
   bool ok = true;
   if constexpr (kSC) {
