@@ -393,8 +393,11 @@ __device__ __forceinline__ double fast_rsqrt(double v, int steps) {
 }
 
 struct FastRed {
-  double red;      // sin/cos reduced angle (reduction.hpp:59-79), NaN for non-finite x
-  double redt;     // tan reduced angle (reduction.hpp:83-93)
+  // sin/cos and tan reduced angles (reduction.hpp:59-79, 83-93) up to sign:
+  // the fused proposed path leaves the fold's sign in them, so every consumer
+  // reads fabs(red) / fabs(redt) (free as FP64 operand modifiers)
+  double red;
+  double redt;
   unsigned neg_s;  // sign-bit masks (0 or 0x80000000) to XOR into the results
   unsigned neg_c;
   unsigned neg_t;
@@ -429,9 +432,11 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
     // when a == RN(2pi*k)), or r within that distance of 2pi (pi), whose fold
     // is <= 0 or smaller than 2^-22 for |x| < 2^30 -- no row bracket accepts
     // either, so those elements take the exact path
-    // (tests/test_capi_host.py::test_markstein_free_floor_is_caught).  |x| >= 2^30 always does (`valid`:
-    // q0 < 2^27, i.e. |x| < 2^27 * 2pi < 2^30; NaN and inf fail it too).
-    o.valid = __double2hiint(q0) < 0x41a00000;
+    // (tests/test_capi_host.py::test_markstein_free_floor_is_caught).
+    // `valid` sends |x| >= 2^24 * 2pi (q0 >= 2^24; NaN, inf) to the exact path:
+    // the argument above needs |x| < 2^30, the fused kernel's shared row
+    // (fast_proposed_core) |x| < 2^27.
+    o.valid = __double2hiint(q0) < 0x41700000;
   }
   const unsigned xs = static_cast<unsigned>(__double2hiint(x)) & 0x80000000u;
   double k = 0.0;       // floor(q1)
@@ -468,7 +473,7 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
       const unsigned chi = p3 ? kHiTwoPi : (p1 ? kHiPi : 0u);
       const unsigned clo = p1 ? kLoPi : 0u;
       const double d = __dsub_rn(r, __hiloint2double(static_cast<int>(chi), static_cast<int>(clo)));
-      o.red = __hiloint2double(__double2hiint(d) & 0x7fffffff, __double2loint(d));  // |d|, integer pipe
+      o.red = d;  // signed: consumers take |red| (operand modifier / integer mask)
       o.valid = o.valid & (static_cast<unsigned>(rh) <= kHiTwoPi);
       // cos sign: q in {1, 2} == (q >= 2) xor (q odd), and q is odd exactly
       // when r - c < 0 (q = 1, 3), so it is the sign bit of d xor p2.
@@ -503,10 +508,21 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
     // reduction.hpp:88-89 (r > pi/2).  Proposed path: high word only; an r
     // with the high word of pi/2 keeps red = r, whose high word no row accepts.
     const bool up = HIW_T ? __double2hiint(r) > kHiHalfPi : r > K.half_pi;
-    o.redt = __dadd_rn(__hiloint2double(up ? static_cast<int>(kHiPi) : 0, up ? static_cast<int>(kLoPi) : 0),
-                       xor_hi(r, up ? 0x80000000u : 0u));
-    o.neg_t = (up ? 0x80000000u : 0u) ^ xs;
-    o.guard = o.redt >= K.guard;
+    const double base = __hiloint2double(up ? static_cast<int>(kHiPi) : 0, up ? static_cast<int>(kLoPi) : 0);
+    if constexpr (NEED_SC && !CLAMP) {
+      // Fused: red_t = |RN(r - base)| (RN(pi - r) = -RN(r - pi)); the sign of
+      // r - base is `up` for every r the sine's checks accept, so it is the
+      // tangent's sign before the odd symmetry.  The cases where r is off by
+      // a period or mis-folded coincide with a sine red the row brackets
+      // reject (r within 2^-19 of a multiple of pi / pi/2).
+      const double d = __dsub_rn(r, base);
+      o.redt = d;  // signed, as red
+      o.neg_t = (static_cast<unsigned>(__double2hiint(d)) & 0x80000000u) ^ xs;
+    } else {
+      o.redt = __dadd_rn(base, xor_hi(r, up ? 0x80000000u : 0u));
+      o.neg_t = (up ? 0x80000000u : 0u) ^ xs;
+    }
+    o.guard = fabs(o.redt) >= K.guard;
   }
   return o;
 }
@@ -547,7 +563,7 @@ __device__ __forceinline__ Out3 fast_proposed_core(double x, const SmemTable& tb
   // the high-word bracket's extra LDS sits on that short kernel's critical path.
   constexpr bool kDbl = !kSC;
   const FastRed fr = fast_reduce<kSC, kT, false, !kDbl>(x);
-  const double key = kSC ? fr.red : fr.redt;
+  const double key = fabs(kSC ? fr.red : fr.redt);
   const unsigned g = static_cast<unsigned>(__double2loint(__fma_rz(key, K.twelve_over_pi, K.two52))) & 7u;
   // Row loads as ld.shared from the table's 32-bit shared address (a generic
   // pointer costs the loop a CTA-window base re-materialisation per element).
@@ -562,18 +578,21 @@ __device__ __forceinline__ Out3 fast_proposed_core(double x, const SmemTable& tb
   const double sZ = __hiloint2double(zq.y, zq.x);
   bool ok = true;
   if constexpr (kSC) {
-    const int h = __double2hiint(fr.red);
+    const int h = __double2hiint(fr.red) & 0x7fffffff;
     ok = fr.valid & (h > zq.z) & (h < zq.w);
   }
   if constexpr (kT && kDbl) {
-    ok = fr.valid & (fr.redt >= s.klo) & (fr.redt < s.khi);
-  } else if constexpr (kT) {
-    const int h = __double2hiint(fr.redt);
-    ok = ok & (h > zq.z) & (h < zq.w);
+    ok = fr.valid & (fabs(fr.redt) >= s.klo) & (fabs(fr.redt) < s.khi);
   }
+  // Fused kernels: the tangent shares the sine's row without a check of its
+  // own.  red and red_t both round the distance from |x| to the nearest
+  // multiple of pi, |red - red_t| <= 2^-52 |x| + 2^-49 < 3e-8 for |x| < 2^27
+  // (`valid`), while every accepted high-word bracket lies >= 5.2e-8 inside
+  // its knots (pi/12's low word 0x382d7365 ulps of 2^-54 is the closest) --
+  // so red_t is in the same segment.  tests/test_capi_host.py::test_shared_row_margin.
   Out3 o{0.0, 0.0, 0.0, 0, 0};
   if constexpr (kSC) {
-    const double red = fr.red;
+    const double red = fabs(fr.red);
     const double rad = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(s.X, red), s.Y), red), sZ);
     const double rs = fast_rsqrt<SQ>(rad, steps);
     if constexpr ((MASK & kSin) != 0)
@@ -582,7 +601,7 @@ __device__ __forceinline__ Out3 fast_proposed_core(double x, const SmemTable& tb
       o.c = xor_hi(__dmul_rn(__dadd_rn(__dmul_rn(s.c, red), s.d), rs), fr.neg_c);
   }
   if constexpr (kT) {
-    const double red = fr.redt;
+    const double red = fabs(fr.redt);
     const double poly = __dadd_rn(__dmul_rn(s.a, red), s.b);
     const double den = __dadd_rn(__dmul_rn(s.c, red), s.d);
     double v;

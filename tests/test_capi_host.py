@@ -141,6 +141,64 @@ def test_markstein_free_floor_is_caught():
     assert checked > 0  # the neighbourhoods do contain floor disagreements
 
 
+def _hi(v):
+    return int(np.float64(v).view(np.uint64) >> np.uint64(32))
+
+
+def test_shared_row_margin(ft):
+    """ft_core.cuh fast_proposed_core: fused kernels give the tangent the
+    sine's segment row without a bracket check of its own.  Pins the two facts
+    that argument rests on: (1) every high-word bracket a row accepts lies at
+    least 5.2e-8 inside its knots, (2) the fused path's red and red_t (kernel
+    operation order, exact FMA) differ by at most 2^-52*a + 2^-49 < 3e-8 for
+    a < 2^27 -- checked on random a and on a near k*pi + knot."""
+    from fractions import Fraction
+
+    T = ft.segment_table()
+    knots = T[42:49]
+    # (1) margins of the high-word brackets (rows 1..5 lower, rows 0..4 upper)
+    margins = []
+    for kn in knots[1:6]:
+        lo_edge = ((np.uint64(_hi(kn) + 1) << np.uint64(32))).view(np.float64)  # smallest accepted above
+        hi_edge = ((np.uint64(_hi(kn)) << np.uint64(32)) - np.uint64(1)).view(np.float64)  # largest accepted below
+        margins += [lo_edge - kn, kn - hi_edge]
+    assert min(margins) > 5.2e-8
+
+    # (2) red vs red_t in the kernel's operation order
+    P = math.pi
+    TWO_PI = 2.0 * P
+    y = 1.0 / TWO_PI
+
+    def fma(a, b, c):
+        return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+    rng = np.random.default_rng(3)
+    a_s = list(rng.uniform(0, 2.0**27, 3000)) + list(rng.uniform(0, 10.0, 1000))
+    ks = rng.integers(0, 2**27 / P, 3000)
+    a_s += [float(k * P + kn + d) for k, kn, d in zip(ks, rng.choice(knots[1:6], 3000), rng.uniform(-1e-7, 1e-7, 3000))]
+    worst = 0.0
+    for a in a_s:
+        a = float(a)
+        if not (0.0 < a < 2.0**27):
+            continue
+        q0 = a * y
+        k = math.floor(q0)
+        r = a - TWO_PI * k
+        rh = _hi(r)
+        p1, p2, p3 = rh > 0x3FF921FB, rh > 0x400921FB, rh > 0x4012D97C
+        c = 2 * P if p3 else (P if p1 else 0.0)
+        red = abs(r - c)
+        rt = a - fma(float(k), TWO_PI, P if p2 else 0.0)
+        up = _hi(rt) > 0x3FF921FB
+        redt = abs(rt - (P if up else 0.0))
+        if red < 2.0**-17 or _hi(red) >= 0x3FF921FB or not (0 <= rh <= 0x401921FB):
+            continue  # rejected by the sine's checks
+        diff = abs(red - redt)
+        assert diff <= 2.0**-52 * a + 2.0**-49
+        worst = max(worst, diff)
+    assert worst < 3e-8
+
+
 def test_invalid_arguments_fail_without_gpu(ft):
     from paper_2502_10831_b200 import _lib
 
