@@ -466,15 +466,16 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
       // so RN(pi - r) = -RN(r - pi) and RN(2pi - r) = -RN(r - 2pi).  A wrong
       // quadrant from the high-word compares puts red within 2^-19 of 0
       // (r ~ pi: same |red|, wrong sine sign) or at/above pi/2 (r ~ pi/2,
-      // 3pi/2); r < 0 and r beyond 2pi's high word (the reference's clamps,
-      // NaN) are caught by `valid`, r sharing 2pi's high word gives
-      // red < 2^-18.  No row bracket accepts red < 2^-17 or hi(red) >=
-      // hi(pi/2) (SmemTable), so all of these take the exact path.
+      // 3pi/2).  For |x| < 2^27 (`valid`) an r outside [0, 2pi) -- the
+      // reference's clamps, or a floor off by one (above) -- is within
+      // 2^-24 of 0 or 2pi (2pi's high word spans 2pi + 2.4e-6), so it folds
+      // to red < 2^-17 too; NaN keeps a NaN high word.  No row bracket accepts
+      // red < 2^-17 or hi(red) >= hi(pi/2) (SmemTable), so all of these take
+      // the exact path.
       const unsigned chi = p3 ? kHiTwoPi : (p1 ? kHiPi : 0u);
       const unsigned clo = p1 ? kLoPi : 0u;
       const double d = __dsub_rn(r, __hiloint2double(static_cast<int>(chi), static_cast<int>(clo)));
       o.red = d;  // signed: consumers take |red| (operand modifier / integer mask)
-      o.valid = o.valid & (static_cast<unsigned>(rh) <= kHiTwoPi);
       // cos sign: q in {1, 2} == (q >= 2) xor (q odd), and q is odd exactly
       // when r - c < 0 (q = 1, 3), so it is the sign bit of d xor p2.
       o.neg_c = (static_cast<unsigned>(__double2hiint(d)) & 0x80000000u) ^ (p2 ? 0x80000000u : 0u);
@@ -509,8 +510,8 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
     // with the high word of pi/2 keeps red = r, whose high word no row accepts.
     const bool up = HIW_T ? __double2hiint(r) > kHiHalfPi : r > K.half_pi;
     const double base = __hiloint2double(up ? static_cast<int>(kHiPi) : 0, up ? static_cast<int>(kLoPi) : 0);
-    if constexpr (NEED_SC && !CLAMP) {
-      // Fused: red_t = |RN(r - base)| (RN(pi - r) = -RN(r - pi)); the sign of
+    if constexpr (HIW_T) {
+      // Proposed path: red_t = |RN(r - base)| (RN(pi - r) = -RN(r - pi)); the sign of
       // r - base is `up` for every r the sine's checks accept, so it is the
       // tangent's sign before the odd symmetry.  The cases where r is off by
       // a period or mis-folded coincide with a sine red the row brackets
