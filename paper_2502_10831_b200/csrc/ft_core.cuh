@@ -652,21 +652,60 @@ __device__ __forceinline__ double taylor_horner(const double* c, int n, double s
   }
 }
 
+// Exact path of fast_taylor: the device restatement of each requested function.
+template <unsigned MASK>
+static __device__ __noinline__ Out3 slow_taylor(double x, int n) {
+  Out3 o{0.0, 0.0, 0.0, 0, 0};
+  if constexpr ((MASK & kSin) != 0) o.s = mirror_taylor(c_taylor, 0, x, n);
+  if constexpr ((MASK & kCos) != 0) o.c = mirror_taylor(c_taylor, 1, x, n);
+  if constexpr ((MASK & kTan) != 0) o.t = mirror_taylor(c_taylor, 2, x, n);
+  return o;
+}
+
 // Fused Taylor sin/cos/tan of one element, n nonzero terms.
-template <int NT, unsigned MASK>
+// With sin or cos in MASK: the proposed path's reduction (fast_reduce, no
+// clamps, no Markstein step, high-word quadrant, signed folds) certified by
+// red's high word -- every case where it can differ from the reference
+// (off-by-one floor, quadrant mis-fold, r outside [0, 2pi), |x| >= 2^24 * 2pi,
+// non-finite x) has red < 2^-17 or hi(red) >= hi(pi/2) (see fast_reduce), and
+// is redone exactly; the tangent shares k and its failure cases (as in
+// fast_proposed_core).  CERT = false, or tan only: the clamped exact reduction
+// (f64 kernels are memory-bound and measured faster without the exact-path
+// branch: 256 vs 246 Gelem/s, cfg4 f64; f32 gains 381 -> 419).
+template <int NT, unsigned MASK, bool CERT = true>
 __device__ __forceinline__ Out3 fast_taylor(double x, int n) {
   constexpr bool kSC = (MASK & (kSin | kCos)) != 0;
   constexpr bool kT = (MASK & kTan) != 0;
-  const FastRed fr = fast_reduce<kSC, kT, true>(x);
   Out3 o{0.0, 0.0, 0.0, 0, 0};
-  if constexpr (kSC) {
+  if constexpr (kSC && !CERT) {
+    const FastRed fr = fast_reduce<true, kT, true>(x);
     const double s2 = __dmul_rn(fr.red, fr.red);
     if constexpr ((MASK & kSin) != 0)
       o.s = xor_hi(__dmul_rn(fr.red, taylor_horner<NT>(c_taylor.sin_c, n, s2)), fr.neg_s);
     if constexpr ((MASK & kCos) != 0)
       o.c = xor_hi(taylor_horner<NT>(c_taylor.cos_c, n, s2), fr.neg_c);
-  }
-  if constexpr (kT) {
+    if constexpr (kT) {
+      const double s2t = __dmul_rn(fr.redt, fr.redt);
+      o.t = xor_hi(__dmul_rn(fr.redt, taylor_horner<NT>(c_taylor.tan_c, n, s2t)), fr.neg_t);
+    }
+  } else if constexpr (kSC) {
+    const FastRed fr = fast_reduce<true, kT, false, true>(x);
+    const int h = __double2hiint(fr.red) & 0x7fffffff;
+    const bool ok = fr.valid & (h > kHiRow0Lo) & (h < kHiHalfPi);
+    const double red = fabs(fr.red);
+    const double s2 = __dmul_rn(red, red);
+    if constexpr ((MASK & kSin) != 0)
+      o.s = xor_hi(__dmul_rn(red, taylor_horner<NT>(c_taylor.sin_c, n, s2)), fr.neg_s);
+    if constexpr ((MASK & kCos) != 0)
+      o.c = xor_hi(taylor_horner<NT>(c_taylor.cos_c, n, s2), fr.neg_c);
+    if constexpr (kT) {
+      const double redt = fabs(fr.redt);
+      const double s2t = __dmul_rn(redt, redt);
+      o.t = xor_hi(__dmul_rn(redt, taylor_horner<NT>(c_taylor.tan_c, n, s2t)), fr.neg_t);
+    }
+    if (!ok) o = slow_taylor<MASK>(x, n);  // rare
+  } else {
+    const FastRed fr = fast_reduce<false, true, true>(x);
     const double s2 = __dmul_rn(fr.redt, fr.redt);
     o.t = xor_hi(__dmul_rn(fr.redt, taylor_horner<NT>(c_taylor.tan_c, n, s2)), fr.neg_t);
   }

@@ -251,12 +251,12 @@ struct ProposedOp {
   __device__ __forceinline__ Out3 slow(double x) const { return slow_proposed_mode<SQ>(x, steps); }
 };
 
-template <int NT, unsigned MASK>
+template <int NT, unsigned MASK, bool CERT>
 struct TaylorOp {
   template <typename T>
   static constexpr int kGroup = 1;
   int n;
-  __device__ __forceinline__ Out3 operator()(double x) const { return fast_taylor<NT, MASK>(x, n); }
+  __device__ __forceinline__ Out3 operator()(double x) const { return fast_taylor<NT, MASK, CERT>(x, n); }
 };
 
 // Device restatement: each function evaluated separately, exactly as the
@@ -296,7 +296,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_proposed(const Eval
 // ---------------- K2 ----------------
 template <typename T, int NT, unsigned MASK>
 __global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_taylor(const EvalArgs a) {
-  stream_map<T, MASK, false, TaylorOp<NT, MASK>, kTmaK2<T>>(a, TaylorOp<NT, MASK>{a.steps});
+  using Op = TaylorOp<NT, MASK, sizeof(T) == 4>;  // certify-or-redo for the instruction-bound f32 kernels
+  stream_map<T, MASK, false, Op, kTmaK2<T>>(a, Op{a.steps});
 }
 
 // ---------------- device restatement ----------------
