@@ -131,12 +131,13 @@ struct FastConsts {
   double twelve_over_pi;  // RN(12/pi): row guess floor(red * 12/pi)
   double two52;           // 2^52: fma.rz(red, 12/pi, 2^52) puts floor() in the low word
   double half;            // 0.5 (FISR Newton step, as a c[][] operand)
+  double inv_pi;          // RN(1/pi) = 2 * RN(1/2pi)
 };
 constexpr FastConsts make_fast_consts() {
   return FastConsts{{kHalfPi, kPi, 3.0 * kHalfPi},
                     0x1.91de2c0cf70aep+0,
                     {kTable.knots[1], kTable.knots[2], kTable.knots[3], kTable.knots[4], kTable.knots[5]},
-                    kPi, kTwoPi, kHalfPi, kInvTwoPi, 12.0 / kPi, 0x1p52, 0.5};
+                    kPi, kTwoPi, kHalfPi, kInvTwoPi, 12.0 / kPi, 0x1p52, 0.5, 2.0 * kInvTwoPi};
 }
 constexpr FastConsts kFast = make_fast_consts();
 
@@ -419,7 +420,10 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
   // q1 = RN(a / 2pi) exactly: y = RN(1/2pi) is within 0.206*2^-53 relative, so
   // q0 = RN(a*y) is within 0.912 ulp of a/2pi and one Markstein correction
   // (exact FMA remainder) rounds to RN(a/2pi).
-  const double q0 = __dmul_rn(a, K.inv_two_pi);
+  // Tan-only proposed kernels need only RN(a/pi)'s stand-in 2*q0, which is
+  // RN(a * RN(1/pi)) exactly (RN(1/pi) = 2 RN(1/2pi)): one DMUL, no doubling.
+  constexpr bool kTanOnly = !NEED_SC && !CLAMP;
+  const double q0 = kTanOnly ? __dmul_rn(a, K.inv_pi) : __dmul_rn(a, K.inv_two_pi);
   double q1 = q0;
   if constexpr (CLAMP) {
     const double rem = __fma_rn(-q0, K.two_pi, a);
@@ -436,7 +440,7 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
     // `valid` sends |x| >= 2^24 * 2pi (q0 >= 2^24; NaN, inf) to the exact path:
     // the argument above needs |x| < 2^30, the fused kernel's shared row
     // (fast_proposed_core) |x| < 2^27.
-    o.valid = __double2hiint(q0) < 0x41700000;
+    o.valid = __double2hiint(q0) < (kTanOnly ? 0x41800000 : 0x41700000);  // (2)q0 < 2^24 (2^25)
   }
   const unsigned xs = static_cast<unsigned>(__double2hiint(x)) & 0x80000000u;
   double k = 0.0;       // floor(q1)
@@ -485,11 +489,10 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
     if constexpr (CLAMP) o.neg_c = (p1 != p3) ? 0x80000000u : 0u;  // q in {1, 2} (reduction.hpp:77)
   }
   if constexpr (NEED_T) {
-    // RN(a/pi) == 2*RN(a/2pi) exactly (2pi is an exact doubling of pi)
-    // Proposed path: 2*q1 as an exponent increment (integer pipe).  Exact for
-    // normal q1; for q1 = 0 or subnormal both forms floor to 0.  Non-finite x
-    // (q1 NaN) gives r = +inf or NaN, whose fold fails every bracket; the
-    // Taylor path (CLAMP, no exact fallback) keeps the DADD so NaN survives.
+    // RN(a/pi) == 2*RN(a/2pi) exactly (2pi is an exact doubling of pi).  The
+    // clamped path doubles the corrected q1; the tan-only proposed path floors
+    // q0 = RN(a*RN(1/pi)) = 2*RN(a*RN(1/2pi)) (an off-by-one floor is rejected
+    // by the bracket, as for the sine).  Non-finite x fails `valid`.
     double r;
     if constexpr (NEED_SC && !CLAMP) {
       // Fused proposed path: floor(RN(a/pi)) = 2k + [r >= pi] for the sine's
@@ -501,8 +504,7 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
       const double s_pi = __hiloint2double(upper ? static_cast<int>(kHiPi) : 0, upper ? static_cast<int>(kLoPi) : 0);
       r = __dsub_rn(a, __fma_rn(k, K.two_pi, s_pi));
     } else {
-      const double q2 = CLAMP ? __dadd_rn(q1, q1)
-                              : __hiloint2double(__double2hiint(q1) + 0x00100000, __double2loint(q1));
+      const double q2 = CLAMP ? __dadd_rn(q1, q1) : q0;  // tan-only: q0 = RN(a * RN(1/pi))
       r = __dsub_rn(a, __dmul_rn(K.pi, floor(q2)));
     }
     if constexpr (CLAMP) r = (r < 0.0 || r >= K.pi) ? 0.0 : r;
@@ -510,12 +512,14 @@ __device__ __forceinline__ FastRed fast_reduce(double x) {
     // with the high word of pi/2 keeps red = r, whose high word no row accepts.
     const bool up = HIW_T ? __double2hiint(r) > kHiHalfPi : r > K.half_pi;
     const double base = __hiloint2double(up ? static_cast<int>(kHiPi) : 0, up ? static_cast<int>(kLoPi) : 0);
-    if constexpr (HIW_T) {
+    if constexpr (!CLAMP) {
       // Proposed path: red_t = |RN(r - base)| (RN(pi - r) = -RN(r - pi)); the sign of
       // r - base is `up` for every r the sine's checks accept, so it is the
-      // tangent's sign before the odd symmetry.  The cases where r is off by
-      // a period or mis-folded coincide with a sine red the row brackets
-      // reject (r within 2^-19 of a multiple of pi / pi/2).
+      // tangent's sign before the odd symmetry.  Fused kernels: the cases
+      // where r is off by a period or mis-folded coincide with a sine red the
+      // row brackets reject (r within 2^-19 of a multiple of pi / pi/2).
+      // Tan-only (exact `up`): r outside [0, pi) is within 2^-24 of 0 or pi
+      // for |x| < 2^25 pi and folds below row 0's bound 2^-17.
       const double d = __dsub_rn(r, base);
       o.redt = d;  // signed, as red
       o.neg_t = (static_cast<unsigned>(__double2hiint(d)) & 0x80000000u) ^ xs;
