@@ -38,9 +38,6 @@ constexpr int kMinBlocks = kTmaK1<T> ? 3 : FT_MINB_F32;
 #ifndef FT_BATCH_SLOW
 #define FT_BATCH_SLOW 1
 #endif
-#ifndef FT_PAIR
-#define FT_PAIR 0  // 1: f32 fused kernels branch once per pair of elements
-#endif
 #ifndef FT_RPF
 #define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
 #endif
@@ -239,7 +236,7 @@ struct ProposedOp {
   // Elements per exact-path branch (see stream_map).
   template <typename T>
   static constexpr int kGroup =
-      FT_BATCH_SLOW == 2 ? 4 : (FT_BATCH_SLOW == 1 && MASK == kTan) ? 4 : (FT_PAIR && sizeof(T) == 4) ? 2 : 1;
+      FT_BATCH_SLOW == 2 ? 4 : (FT_BATCH_SLOW == 1 && MASK == kTan) ? 4 : 1;
   const SmemTable* tb;
   int steps;
   __device__ __forceinline__ Out3 operator()(double x) const {
