@@ -13,8 +13,8 @@ namespace {
 
 constexpr int kThreads = 256;
 // Output path per dtype.  f64 (32 B/elem at cfg2, memory-bound): block tiles
-// written by TMA bulk stores at 3 blocks/SM -- equal to per-thread stores
-// under the sustained power cap and 12% faster per launch (6.16 vs 5.51 TB/s).
+// written by TMA bulk stores, compiled for >= 3 blocks/SM (60 registers: 4 are
+// resident) -- 12% faster per launch than per-thread stores (6.16 vs 5.51 TB/s).
 // f32 (16 B/elem, instruction-bound): per-thread streaming stores at 4 blocks/SM
 // (the TMA path costs it 3-5%).  profiles/r01_k1_variants.json.
 #ifndef FT_TMA_F64

@@ -108,6 +108,46 @@ def test_k1_adversarial_quotients(ft):
         check_against(xf, out, O.proposed(xf, 7, m, s, seg=True))
 
 
+def test_certify_or_redo_boundaries(ft):
+    """The fast paths' certificates (ft_core.cuh fast_reduce / fast_proposed_core
+    / fast_taylor): inputs straddling each bound they rest on must still return
+    the reference's bits in every output mask, f32 and f64, proposed and Taylor:
+    |x| around the `valid` limit 2^24*2pi (= 2^25*pi for tan-only), odd and even
+    multiples of pi and pi/2 up to that limit (tangent floor taken from the
+    sine's k, off-by-one floors), and reduced angles around row 0's bound 2^-17."""
+    rng = np.random.default_rng(17)
+    P = math.pi
+    lim = 2.0**24 * 2 * P
+    parts = [lim * (1 + rng.uniform(-1e-3, 1e-3, 20000)),
+             lim + np.arange(-2000, 2000) * np.spacing(lim)]
+    k = np.concatenate([rng.integers(1, int(lim / P), 30000), np.arange(1, 3000)]).astype(np.float64)
+    for mult in (P, 0.5 * P):
+        b = k * mult
+        b = b[b < 1.05 * lim]
+        parts += [b + d * np.spacing(b) for d in (-3, -1, 0, 1, 3)]
+    kk = np.arange(0, 64).astype(np.float64)
+    for e in (-17.0, -16.0, -18.0):
+        d = 2.0**e * (1 + rng.uniform(-1e-3, 1e-3, kk.size))
+        parts += [kk * P + d, kk * P - d, kk * P + 0.5 * P + d]
+    x = np.concatenate(parts)
+    x = np.concatenate([x, -x])
+    for dtype in (np.float64, np.float32):
+        xd = x.astype(dtype)
+        for mask in range(1, 8):
+            out = ft.proposed_eval(dev(xd), mask, seg=mask == 7)
+            torch.cuda.synchronize()
+            ref = O.proposed(xd, mask, seg=mask == 7)
+            fns = [f for j, f in enumerate(("sin", "cos", "tan")) if mask & (1 << j)]
+            check_against(xd, out, ref, fns=fns, seg=mask == 7)
+        for mask in (3, 7, 4):
+            out = ft.taylor_eval(dev(xd), 5, mask)
+            torch.cuda.synchronize()
+            ref = O.taylor(xd, 5, mask)
+            for j, f in enumerate(("sin", "cos", "tan")):
+                if mask & (1 << j):
+                    assert same_bits(host(out[f]), ref[f]), (dtype, mask, f)
+
+
 def test_k1_hiword_zones(ft):
     """The fast path compares high words only (quadrant, tan fold, row bracket,
     ft_core.cuh fast_reduce/SmemTable): inputs whose r or red shares its high
