@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -432,8 +433,17 @@ unsigned persistent_blocks(const void* fn, int threads, std::size_t work_items) 
   }
   if (occ < 1) occ = 1;
   if (sms < 1) sms = 1;
+  // Four waves of resident blocks rather than exactly one: blocks that finish
+  // early are backfilled, which trims the tail of the short launches (cfg1
+  // +1.6%, cfg3 +1.8%, cfg2 +0.4% vs one wave; tools/gridmult_sweep.sh,
+  // profiles/r01_k1_variants.json).  FT_GRID_MULT overrides it for experiments.
+  static const int mult = [] {
+    const char* e = std::getenv("FT_GRID_MULT");
+    const int m = e ? std::atoi(e) : 4;
+    return m >= 1 ? m : 1;
+  }();
   const std::size_t need = (work_items + threads - 1) / threads;
-  const std::size_t full = static_cast<std::size_t>(occ) * sms;
+  const std::size_t full = static_cast<std::size_t>(occ) * sms * mult;
   return static_cast<unsigned>(std::max<std::size_t>(1, std::min(need, full)));
 }
 
