@@ -32,6 +32,13 @@ constexpr bool kTmaK2 = (sizeof(T) == 8 && FT_TMA_F64) || (sizeof(T) == 4 && FT_
 #endif
 template <typename T>
 constexpr int kMinBlocks = kTmaK1<T> ? 3 : FT_MINB_F32;
+// K2 f32 (Taylor, 48 registers suffice): 5 resident blocks/SM measured +3.5%
+// over 4 (cfg4 f32 449.7 vs 434.2 Gelem/s); K1 f32 loses 2-6% at 5.
+#ifndef FT_MINB_K2_F32
+#define FT_MINB_K2_F32 5
+#endif
+template <typename T>
+constexpr int kMinBlocksK2 = kTmaK2<T> ? 3 : (sizeof(T) == 4 ? FT_MINB_K2_F32 : FT_MINB_F32);
 // Where the exact-path branch sits: 0 one per element; 1 one per vector for
 // tan-only kernels (cfg3 +5%; the fused kernels lose 10% to the extra live
 // registers at the 64-register cap); 2 one per vector everywhere.
@@ -292,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_proposed(const Eval
 
 // ---------------- K2 ----------------
 template <typename T, int NT, unsigned MASK>
-__global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_taylor(const EvalArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinBlocksK2<T>) k_taylor(const EvalArgs a) {
   using Op = TaylorOp<NT, MASK, sizeof(T) == 4>;  // certify-or-redo for the instruction-bound f32 kernels
   stream_map<T, MASK, false, Op, kTmaK2<T>>(a, Op{a.steps});
 }
