@@ -32,10 +32,11 @@ constexpr bool kTmaK2 = (sizeof(T) == 8 && FT_TMA_F64) || (sizeof(T) == 4 && FT_
 #endif
 template <typename T>
 constexpr int kMinBlocks = kTmaK1<T> ? 3 : FT_MINB_F32;
-// K2 f32 (Taylor, 48 registers suffice): 5 resident blocks/SM measured +3.5%
-// over 4 (cfg4 f32 449.7 vs 434.2 Gelem/s); K1 f32 loses 2-6% at 5.
+// K2 f32 (Taylor, 40 registers suffice): 6 resident blocks/SM measured +4.8%
+// over 4 (cfg4 f32: 4 -> 5 -> 6 blocks 434 -> 449 -> 454 Gelem/s; 8 spills);
+// K1 f32 loses 2-6% at 5.
 #ifndef FT_MINB_K2_F32
-#define FT_MINB_K2_F32 5
+#define FT_MINB_K2_F32 6
 #endif
 template <typename T>
 constexpr int kMinBlocksK2 = kTmaK2<T> ? 3 : (sizeof(T) == 4 ? FT_MINB_K2_F32 : FT_MINB_F32);
