@@ -83,7 +83,14 @@ inline std::vector<double> proposed_tan_batch(std::span<const double> xs, SqrtMo
   return out;
 }
 
-// f32 overloads: (float)proposed_*((double)x), element for element.
+// f32 evaluation policy (process-wide).  Default F32Policy::ulp2: within 2 ulp
+// of (float)proposed_*((double)x) with the identical segment choice (checked on
+// all 2^32 floats); F32Policy::bitwise: bit-identical to it.
+enum class F32Policy : int { ulp2 = FT_F32_ULP2, bitwise = FT_F32_BITWISE };
+inline void set_f32_policy(F32Policy p) { check(ft_set_f32_policy(static_cast<int>(p))); }
+inline F32Policy f32_policy() { return static_cast<F32Policy>(ft_get_f32_policy()); }
+
+// f32 overloads: (float)proposed_*((double)x) per element, at the f32 policy.
 inline std::vector<float> proposed_sin_batch(std::span<const float> xs, SqrtMode mode = {}) {
   std::vector<float> out(xs.size());
   check(ft_proposed_batch_host(FT_F32, xs.data(), xs.size(), kSin, to_c(mode), out.data(), nullptr, nullptr));

@@ -21,9 +21,12 @@
  *   - Every other entry point takes DEVICE pointers on the current CUDA device
  *     and is asynchronous on `stream` (a cudaStream_t; NULL = legacy default
  *     stream).  Reentrant per stream.
- *   - Results are bitwise equal to the reference: f64 outputs are identical
- *     to proposed_*(x); f32 inputs are promoted exactly, evaluated in binary64
- *     and rounded once, i.e. identical to (float)proposed_*((double)x).
+ *   - f64 results are bitwise equal to the reference: identical to
+ *     proposed_*(x).  f32 inputs are compared with (float)proposed_*((double)x)
+ *     (the reference is double-only): under the default policy FT_F32_ULP2 the
+ *     f32 outputs are within 2 ulp of it with the identical segment choice
+ *     (the north-star tolerance; all 2^32 inputs are checked in the GPU
+ *     tests); under FT_F32_BITWISE they are bit-identical to it.
  *   - Non-finite x yields a quiet NaN (reduction.hpp:60-62); tan inside the
  *     pole window |red - pi/2| < 1e-3 yields a signed infinity (kernels.hpp:62-64).
  */
@@ -37,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FT_ABI_VERSION 1
+#define FT_ABI_VERSION 2
 
 typedef enum ft_status {
   FT_OK = 0,
@@ -88,6 +91,7 @@ typedef struct ft_stats {
   double max_rel_vs_libm[3];    /* |libm| > 1e-12 guard    */
   double sum_abs_vs_libm[3];
   double sum_rel_vs_libm[3];
+  uint64_t n_bit_mismatch[3];   /* raw bit patterns differ (NaNs canonical; sees +0 vs -0) */
 } ft_stats;
 
 /* ---- host-pointer entry points: the reference batch API (kernels.hpp:84-94) ---- */
@@ -104,6 +108,16 @@ int ft_proposed_batch_host(ft_dtype dtype, const void* x, size_t n, unsigned mas
                            ft_sqrt_mode mode, void* sin_out, void* cos_out, void* tan_out);
 int ft_taylor_batch_host(ft_dtype dtype, const void* x, size_t n, unsigned mask, int n_terms,
                          void* sin_out, void* cos_out, void* tan_out);
+
+/* f32 evaluation policy (process-wide; default FT_F32_ULP2).
+ *   FT_F32_ULP2     <= 2 ulp of (float)proposed_*((double)x), identical segment
+ *                   choice; one signed reduction and FMA-contracted evaluation
+ *                   for |x| < 2^16, bit-exact elsewhere.
+ *   FT_F32_BITWISE  bit-identical to (float)proposed_*((double)x).
+ * Taylor f32 calls follow it for n_terms 5, 7 and 9.  f64 is always bitwise. */
+typedef enum ft_f32_policy { FT_F32_ULP2 = 0, FT_F32_BITWISE = 1 } ft_f32_policy;
+int ft_set_f32_policy(int policy);
+int ft_get_f32_policy(void);
 
 /* Number of GPUs the host-pointer entry points spread one call over: arrays of
  * at least 4 Mi elements are split into that many contiguous shards, each
@@ -169,6 +183,20 @@ int ft_taylor_coeffs(double* sin9, double* cos9, double* tan9);
  * guard found by host bisection against IEEE division/subtraction; out8[4..7]
  * = the same constants as compiled into the kernels (must be identical). */
 int ft_thresholds(double* out8);
+/* The segment table as held in device constant memory, read back from the GPU
+ * (same layout as ft_segment_table).  unit: 0 = the K1/K2 kernels' copy, 1 =
+ * K3's, 2 = K4/K5's, 3 = the C-ABI unit's.  Synchronous. */
+int ft_device_const_table(int unit, double* out49);
+/* The shared-memory segment rows a K1 block stages, copied out by a kernel
+ * (8 rows x 80 bytes: a,b,c,d,X,Y,Z as doubles, the bracket's two high words
+ * as int32, the exact bracket as two doubles).  kind 0 = bit-exact rows,
+ * 1..7 = the relaxed f32 rows for that output mask.  Synchronous. */
+int ft_device_rows(int kind, void* out640);
+/* Free the host-pointer pipeline (streams, device slots, pinned staging) and
+ * the L2-flush buffer of `device` (-1: every device).  They are re-created on
+ * demand by the next call.  Not to be called concurrently with host-pointer
+ * calls on that device. */
+int ft_release(int device);
 /* Number of K1/K2/K3/K4/K5 launches issued by this process so far. */
 uint64_t ft_launch_count(void);
 const char* ft_last_error_string(void);

@@ -94,7 +94,26 @@ def ref() -> C.CDLL:
     lib.ref_reduce.argtypes = [i, d, C.POINTER(d), C.POINTER(d)]
     lib.ref_scalar.restype = d
     lib.ref_scalar.argtypes = [i, d, i, i]
+    lib.ref_check_f32_range.restype = i
+    lib.ref_check_f32_range.argtypes = [C.c_uint32, sz, i, i, vp, vp, vp, vp, vp, vp, i]
     return lib
+
+
+def ref_check_f32_range(start: int, got: dict, method: int = FISR, steps: int = 1,
+                        threads: int | None = None) -> dict:
+    """The unmodified reference on the float inputs with bit patterns start ..
+    start+n-1 (n = len of the given arrays), compared with got['sin'/'cos'/'tan']
+    (float32 host arrays) and optionally got['seg_sc'/'seg_t'] (uint8)."""
+    arrs = [got.get(k) for k in ("sin", "cos", "tan", "seg_sc", "seg_t")]
+    n = next(a.size for a in arrs if a is not None)
+    for a in arrs:
+        assert a is None or (a.size == n and a.flags.c_contiguous)
+    out = np.zeros(11, np.uint64)
+    rc = ref().ref_check_f32_range(start & 0xFFFFFFFF, n, method, steps, *[_p(a) for a in arrs],
+                                   out.ctypes.data, threads or ncpu())
+    assert rc == 0
+    o = [int(v) for v in out]
+    return {"max_ulp": o[0:3], "n_bit_mismatch": o[3:6], "n_over_2ulp": o[6:9], "seg_mismatch": o[9:11]}
 
 
 def _p(a):

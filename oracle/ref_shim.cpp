@@ -8,6 +8,8 @@
 //   * bench.py can time the reference's own CPU path as the baseline
 //     ("cpu_baseline.kind": "reference").
 // The output lands in oracle/_ref/ (git-ignored, travels to the GPU box).
+#include <array>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <span>
@@ -60,9 +62,85 @@ void run_threads(const T* x, std::size_t n, unsigned mask, fasttrig::SqrtMode mo
   for (auto& th : pool) th.join();
 }
 
+// float ulp distance on the ordered integer line (+0 and -0 coincide; NaN vs
+// NaN is 0, NaN vs number is "infinite").
+std::uint64_t ulp_f32(float a, float b) {
+  const bool na = a != a, nb = b != b;
+  if (na || nb) return (na && nb) ? 0 : ~0ull;
+  std::int32_t ia, ib;
+  std::memcpy(&ia, &a, 4);
+  std::memcpy(&ib, &b, 4);
+  const std::int64_t oa = ia < 0 ? -static_cast<std::int64_t>(ia & 0x7fffffff) : ia;
+  const std::int64_t ob = ib < 0 ? -static_cast<std::int64_t>(ib & 0x7fffffff) : ib;
+  return static_cast<std::uint64_t>(oa > ob ? oa - ob : ob - oa);
+}
+
+std::uint32_t canon_bits(float v) {
+  std::uint32_t u;
+  std::memcpy(&u, &v, 4);
+  return v != v ? 0x7fc00000u : u;
+}
+
 }  // namespace
 
 extern "C" {
+
+// Exhaustive-range checker: for the float inputs whose bit patterns are
+// start, start+1, ..., start+n-1 (mod 2^32), evaluates the reference
+// (float)proposed_*((double)x) and compares it with got_{sin,cos,tan} (any may
+// be NULL) and, when given, the segment choices seg_sc / seg_t.
+// out[0..2] max ulp, out[3..5] raw-bit mismatches (NaNs canonical), out[6..8]
+// elements over 2 ulp, out[9..10] segment mismatches (sin/cos, tan).
+int ref_check_f32_range(std::uint32_t start, std::size_t n, int method, int steps,
+                        const float* got_s, const float* got_c, const float* got_t,
+                        const std::uint8_t* seg_sc, const std::uint8_t* seg_t, std::uint64_t* out,
+                        int nthreads) {
+  const auto mode = make_mode(method, steps);
+  if (nthreads < 1) nthreads = 1;
+  std::vector<std::array<std::uint64_t, 11>> acc(static_cast<std::size_t>(nthreads));
+  auto work = [&](int k) {
+    std::array<std::uint64_t, 11> a{};
+    const std::size_t lo = n * k / nthreads, hi = n * (k + 1) / nthreads;
+    const float* got[3] = {got_s, got_c, got_t};
+    for (std::size_t i = lo; i < hi; ++i) {
+      const std::uint32_t b = start + static_cast<std::uint32_t>(i);
+      float xf;
+      std::memcpy(&xf, &b, 4);
+      const double x = static_cast<double>(xf);
+      for (int j = 0; j < 3; ++j) {
+        if (!got[j]) continue;
+        const double r = j == 0 ? fasttrig::proposed_sin(x, mode)
+                         : j == 1 ? fasttrig::proposed_cos(x, mode)
+                                  : fasttrig::proposed_tan(x, mode);
+        const float rf = static_cast<float>(r), g = got[j][i];
+        const std::uint64_t u = ulp_f32(g, rf);
+        a[j] = u > a[j] ? u : a[j];
+        a[3 + j] += canon_bits(g) != canon_bits(rf);
+        a[6 + j] += u > 2;
+      }
+      if (seg_sc) a[9] += seg_sc[i] != static_cast<std::uint8_t>(fasttrig::segment_index(fasttrig::reduce_sin(x).red));
+      if (seg_t) {
+        const fasttrig::ReducedAngle ra = fasttrig::reduce_tan(x);
+        const std::uint8_t want = std::fabs(ra.red - fasttrig::detail::half_pi) < fasttrig::tan_pole_guard
+                                      ? 255
+                                      : static_cast<std::uint8_t>(fasttrig::segment_index(ra.red));
+        a[10] += seg_t[i] != want;
+      }
+    }
+    acc[static_cast<std::size_t>(k)] = a;
+  };
+  std::vector<std::thread> pool;
+  for (int k = 1; k < nthreads; ++k) pool.emplace_back(work, k);
+  work(0);
+  for (auto& th : pool) th.join();
+  for (int j = 0; j < 11; ++j) out[j] = 0;
+  for (const auto& a : acc) {
+    for (int j = 0; j < 3; ++j) out[j] = a[j] > out[j] ? a[j] : out[j];
+    for (int j = 3; j < 11; ++j) out[j] += a[j];
+  }
+  return 0;
+}
+
 
 // Scalar reference calls (kernels.hpp:46-67) on pre-allocated outputs,
 // partitioned contiguously over `nthreads` host threads.

@@ -10,7 +10,11 @@ from .fasttrig import (  # noqa: F401
     SIN,
     TAN,
     SqrtMode,
+    device_const_table,
+    device_rows,
     gen_inputs,
+    f32_policy,
+    get_f32_policy,
     get_host_devices,
     l2_flush,
     launch_count,
@@ -21,7 +25,9 @@ from .fasttrig import (  # noqa: F401
     proposed_eval,
     proposed_sin_batch,
     proposed_tan_batch,
+    release,
     segment_table,
+    set_f32_policy,
     set_host_devices,
     taylor_batch,
     taylor_coeffs,

@@ -19,15 +19,18 @@ FT_F32, FT_F64 = 0, 1
 FT_OUT_SIN, FT_OUT_COS, FT_OUT_TAN = 1, 2, 4
 FT_SQRT_EXACT, FT_SQRT_FISR = 0, 1
 FT_DIST_UNIFORM, FT_DIST_TAN_STRESS = 0, 1
+FT_F32_ULP2, FT_F32_BITWISE = 0, 1
 
-# Every symbol include/fasttrig_b200.h declares (checked by tests/test_capi_symbols.py).
+# Every symbol include/fasttrig_b200.h declares (checked by
+# tests/test_capi_host.py::test_exports_every_declared_symbol).
 EXPORTS = (
     "ft_proposed_sin_batch", "ft_proposed_cos_batch", "ft_proposed_tan_batch",
     "ft_proposed_batch_host", "ft_taylor_batch_host", "ft_proposed_eval", "ft_proposed_eval_seg",
     "ft_taylor_eval", "ft_mirror_eval", "ft_parity_reduce", "ft_stats_reset", "ft_gen_inputs",
     "ft_l2_flush", "ft_host_alloc", "ft_host_free", "ft_segment_table", "ft_taylor_coeffs",
     "ft_thresholds", "ft_launch_count", "ft_last_error_string", "ft_abi_version",
-    "ft_set_host_devices", "ft_get_host_devices",
+    "ft_set_host_devices", "ft_get_host_devices", "ft_set_f32_policy", "ft_get_f32_policy",
+    "ft_device_const_table", "ft_device_rows", "ft_release",
 )
 
 
@@ -52,6 +55,7 @@ class StatsC(C.Structure):
         ("max_rel_vs_libm", C.c_double * 3),
         ("sum_abs_vs_libm", C.c_double * 3),
         ("sum_rel_vs_libm", C.c_double * 3),
+        ("n_bit_mismatch", C.c_uint64 * 3),
     ]
 
 
@@ -104,6 +108,10 @@ def lib() -> C.CDLL:
             "ft_taylor_coeffs": [vp, vp, vp],
             "ft_thresholds": [vp],
             "ft_set_host_devices": [i32],
+            "ft_set_f32_policy": [i32],
+            "ft_device_const_table": [i32, vp],
+            "ft_device_rows": [i32, vp],
+            "ft_release": [i32],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -117,6 +125,8 @@ def lib() -> C.CDLL:
         L.ft_abi_version.argtypes = []
         L.ft_get_host_devices.restype = C.c_int
         L.ft_get_host_devices.argtypes = []
+        L.ft_get_f32_policy.restype = C.c_int
+        L.ft_get_f32_policy.argtypes = []
         _lib = L
         return L
 

@@ -82,14 +82,26 @@ const Thresholds& thresholds() {
 }
 
 // ---- device info ----
+constexpr int kMaxDevices = 128;
 std::mutex g_mu;
 std::unordered_map<const void*, int> g_occ;  // kernel -> resident blocks/SM
-int g_sms[128] = {0};
+int g_sms[kMaxDevices] = {0};
 
-int current_device() {
-  int d = 0;
-  cudaGetDevice(&d);
-  return d;
+// The calling thread's CUDA device, or -1 (with the CUDA error in *err) when
+// the runtime cannot report one.
+int current_device(cudaError_t* err = nullptr) {
+  int d = -1;
+  const cudaError_t e = cudaGetDevice(&d);
+  if (err) *err = e;
+  return e == cudaSuccess ? d : -1;
+}
+
+int device_or_fail(int* dev) {
+  cudaError_t e;
+  *dev = current_device(&e);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  if (*dev >= kMaxDevices) return fail(FT_ERR_CUDA, "device index >= 128 is not supported");
+  return FT_OK;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
@@ -142,7 +154,7 @@ struct HostPipe {
   void* buf[kPipe][4]{};  // x, sin, cos, tan
   std::size_t cap_bytes = 0;
 };
-HostPipe g_pipe[128];
+HostPipe g_pipe[kMaxDevices];
 
 int pipe_reserve(HostPipe& p, std::size_t bytes) {
   if (!p.init) {
@@ -177,7 +189,7 @@ struct Staging {
   cudaEvent_t done[kPipe]{};
   std::size_t cap_bytes = 0;
 };
-Staging g_stage[128];
+Staging g_stage[kMaxDevices];
 
 bool host_pinned(const void* p) {
   if (!p) return true;
@@ -251,8 +263,8 @@ int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* 
   // 4 Mi elements per chunk: short pipeline fill/drain (2.21 vs 2.18 Gelem/s
   // for 8 Mi on 2^26 f64 elements; tools/hp_chunks.sh)
   const std::size_t chunk = std::size_t(1) << 22;
-  const int dev = current_device();
-  if (dev < 0 || dev >= 128) return fail(FT_ERR_CUDA, "device index out of range");
+  int dev = 0;
+  if (const int rc = device_or_fail(&dev)) return rc;
   HostPipe& p = g_pipe[dev];
   std::lock_guard<std::mutex> lk(p.mu);
   int rc = pipe_reserve(p, std::max(chunk, kStageChunk) * es);  // device slots serve both paths
@@ -378,7 +390,8 @@ int host_sharded(int dtype, const void* x, std::size_t n, unsigned mask, void* c
   const std::size_t G = std::min<std::size_t>(static_cast<std::size_t>(want), std::max<std::size_t>(1, n / kMinShard));
   if (G <= 1) return host_pipeline(dtype, x, n, mask, out, launch);
   const std::size_t es = dtype == FT_F32 ? 4 : 8;
-  const int base = current_device();
+  int base = 0;
+  if (const int rc = device_or_fail(&base)) return rc;
   std::vector<int> rcs(G, FT_OK);
   std::vector<std::string> errs(G);
   std::vector<std::thread> th;
@@ -410,12 +423,16 @@ struct FlushBuf {
   std::size_t bytes = 0;
   unsigned tick = 0;
 };
-FlushBuf g_flush[128];
+FlushBuf g_flush[kMaxDevices];
 
 }  // namespace
 
-unsigned persistent_blocks(const void* fn, int threads, std::size_t work_items) {
-  const int dev = current_device();
+cudaError_t persistent_blocks(const void* fn, int threads, std::size_t work_items, unsigned* blocks,
+                              int waves) {
+  cudaError_t e;
+  const int dev = current_device(&e);
+  if (e != cudaSuccess) return e;
+  if (dev >= kMaxDevices) return cudaErrorInvalidDevice;
   int occ = 0, sms = 0;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -423,31 +440,38 @@ unsigned persistent_blocks(const void* fn, int threads, std::size_t work_items) 
     if (it != g_occ.end()) {
       occ = it->second;
     } else {
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0) != cudaSuccess) occ = 1;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0);
+      if (e != cudaSuccess) return e;
+      if (occ < 1) return cudaErrorInvalidConfiguration;  // the kernel cannot be resident at all
       g_occ[fn] = occ;
     }
-    if (dev >= 0 && dev < 128) {
-      if (!g_sms[dev]) cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
-      sms = g_sms[dev];
+    if (!g_sms[dev]) {
+      e = cudaDeviceGetAttribute(&g_sms[dev], cudaDevAttrMultiProcessorCount, dev);
+      if (e != cudaSuccess) return e;
     }
+    sms = g_sms[dev];
   }
-  if (occ < 1) occ = 1;
-  if (sms < 1) sms = 1;
   // Four waves of resident blocks rather than exactly one: blocks that finish
   // early are backfilled, which trims the tail of the short launches (cfg1
   // +1.6%, cfg3 +1.8%, cfg2 +0.4% vs one wave; tools/gridmult_sweep.sh,
   // profiles/r01_k1_variants.json).  FT_GRID_MULT overrides it for experiments.
   static const int mult = [] {
-    const char* e = std::getenv("FT_GRID_MULT");
-    const int m = e ? std::atoi(e) : 4;
+    const char* env = std::getenv("FT_GRID_MULT");
+    const int m = env ? std::atoi(env) : 4;
     return m >= 1 ? m : 1;
   }();
   const std::size_t need = (work_items + threads - 1) / threads;
-  const std::size_t full = static_cast<std::size_t>(occ) * sms * mult;
-  return static_cast<unsigned>(std::max<std::size_t>(1, std::min(need, full)));
+  const std::size_t full = static_cast<std::size_t>(occ) * sms * (waves > 0 ? waves : mult);
+  *blocks = static_cast<unsigned>(std::max<std::size_t>(1, std::min(need, full)));
+  return cudaSuccess;
 }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+std::atomic<int> g_f32_policy{FT_F32_ULP2};
+}
+int f32_policy() { return g_f32_policy.load(std::memory_order_relaxed); }
 
 }  // namespace ft
 
@@ -594,13 +618,14 @@ int ft_gen_inputs(ft_dtype dtype, int dist, double lo, double hi, uint64_t seed,
 }
 
 int ft_l2_flush(void* stream) {
-  const int dev = current_device();
-  if (dev < 0 || dev >= 128) return fail(FT_ERR_CUDA, "device index out of range");
+  int dev = 0;
+  if (const int rc = device_or_fail(&dev)) return rc;
   FlushBuf& f = g_flush[dev];
   std::lock_guard<std::mutex> lk(f.mu);
   if (!f.p) {
     int l2 = 0;
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    const cudaError_t ea = cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    if (ea != cudaSuccess) return cuda_status(ea, "cudaDeviceGetAttribute(L2 size)");
     f.bytes = std::max<std::size_t>(2 * static_cast<std::size_t>(l2), std::size_t(64) << 20);
     cudaError_t e = cudaMalloc(&f.p, f.bytes);
     if (e != cudaSuccess) {
@@ -610,6 +635,102 @@ int ft_l2_flush(void* stream) {
   }
   return cuda_status(launch_fill(f.p, f.bytes, ++f.tick, as_stream(stream)), "ft_l2_flush");
 }
+
+int ft_device_const_table(int unit, double* out49) {
+  if (!out49) return fail(FT_ERR_INVALID_ARG, "out is NULL");
+  Table t{};
+  cudaError_t e;
+  switch (unit) {
+    case 0: e = read_const_table_eval(&t); break;
+    case 1: e = read_const_table_check(&t); break;
+    case 2: e = read_const_table_gen(&t); break;
+    case 3: e = cudaMemcpyFromSymbol(&t, c_table, sizeof(Table)); break;
+    default: return fail(FT_ERR_INVALID_ARG, "unit must be 0 (K1/K2), 1 (K3), 2 (K4/K5) or 3 (C-ABI)");
+  }
+  if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyFromSymbol(c_table)");
+  for (int k = 0; k < 6; ++k) {
+    const Coeffs& c = t.seg[k];
+    const double v[7] = {c.a, c.b, c.c, c.d, c.X, c.Y, c.Z};
+    for (int j = 0; j < 7; ++j) out49[k * 7 + j] = v[j];
+  }
+  for (int j = 0; j < 7; ++j) out49[42 + j] = t.knots[j];
+  return FT_OK;
+}
+
+int ft_device_rows(int kind, void* out640) {
+  if (!out640) return fail(FT_ERR_INVALID_ARG, "out is NULL");
+  if (kind < 0 || kind > 7) return fail(FT_ERR_INVALID_ARG, "kind must be 0 (bit-exact) or an f32 mask 1..7");
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 640);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMalloc(rows)");
+  e = launch_dump_rows(kind, d, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(out640, d, 640, cudaMemcpyDeviceToHost);
+  const cudaError_t ef = cudaFree(d);
+  if (e != cudaSuccess) return cuda_status(e, "ft_device_rows");
+  return cuda_status(ef, "cudaFree(rows)");
+}
+
+int ft_release(int device) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDeviceCount");
+  if (device >= ndev || device < -1) return fail(FT_ERR_INVALID_ARG, "device out of range");
+  const int lo = device < 0 ? 0 : device, hi = device < 0 ? std::min(ndev, kMaxDevices) : device + 1;
+  cudaError_t first = cudaSuccess;
+  auto keep = [&](cudaError_t r) {
+    if (first == cudaSuccess && r != cudaSuccess) first = r;
+  };
+  for (int d = lo; d < hi; ++d) {
+    {
+      HostPipe& p = g_pipe[d];
+      std::lock_guard<std::mutex> lk(p.mu);
+      for (auto& st : p.st)
+        if (st) {
+          keep(cudaStreamSynchronize(st));
+          keep(cudaStreamDestroy(st));
+          st = nullptr;
+        }
+      for (auto& row : p.buf)
+        for (auto& b : row)
+          if (b) {
+            keep(cudaFree(b));
+            b = nullptr;
+          }
+      p.cap_bytes = 0;
+      p.init = false;
+      Staging& g = g_stage[d];  // used only under the pipeline lock
+      for (auto& row : g.pin)
+        for (auto& b : row)
+          if (b) {
+            keep(cudaFreeHost(b));
+            b = nullptr;
+          }
+      for (auto& ev : g.done)
+        if (ev) {
+          keep(cudaEventDestroy(ev));
+          ev = nullptr;
+        }
+      g.cap_bytes = 0;
+    }
+    FlushBuf& f = g_flush[d];
+    std::lock_guard<std::mutex> lk(f.mu);
+    if (f.p) {
+      keep(cudaFree(f.p));
+      f.p = nullptr;
+      f.bytes = 0;
+    }
+  }
+  return cuda_status(first, "ft_release");
+}
+
+int ft_set_f32_policy(int policy) {
+  if (policy != FT_F32_ULP2 && policy != FT_F32_BITWISE)
+    return fail(FT_ERR_INVALID_ARG, "f32 policy must be FT_F32_ULP2 (0) or FT_F32_BITWISE (1)");
+  g_f32_policy.store(policy);
+  return FT_OK;
+}
+
+int ft_get_f32_policy(void) { return g_f32_policy.load(); }
 
 int ft_set_host_devices(int n) {
   g_host_devices.store(n);

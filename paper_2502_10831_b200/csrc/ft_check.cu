@@ -67,6 +67,7 @@ struct Acc {
   std::uint64_t n = 0;
   std::uint64_t max_ulp[3] = {0, 0, 0}, over[3] = {0, 0, 0}, seg_mm[2] = {0, 0};
   std::uint64_t inf[3] = {0, 0, 0}, nan[3] = {0, 0, 0}, nfin[3] = {0, 0, 0}, cks[3] = {0, 0, 0};
+  std::uint64_t bits[3] = {0, 0, 0};  // raw-bit mismatches (ulp_dist treats +0 and -0 as equal)
   // non-negative doubles kept as bit patterns (ordered like the values)
   std::uint64_t max_or[3] = {0, 0, 0}, max_abs[3] = {0, 0, 0}, max_rel[3] = {0, 0, 0};
   double sum_abs[3] = {0, 0, 0}, sum_rel[3] = {0, 0, 0};
@@ -102,11 +103,14 @@ __global__ void __launch_bounds__(kThreads) k_check(const CheckArgs a) {
       const std::uint64_t u = ulp_dist<T>(got, want);
       acc.max_ulp[j] = umax(acc.max_ulp[j], u);
       acc.over[j] += u > a.ulp_tol;
+      const std::uint64_t bg = isnan(got) ? Bits<T>::kNaN : Bits<T>::raw(got);
+      const std::uint64_t bw = isnan(want) ? Bits<T>::kNaN : Bits<T>::raw(want);
+      acc.bits[j] += bg != bw;
       const double g = static_cast<double>(got), w = static_cast<double>(want);
       if (isfinite(g) && isfinite(w)) acc.max_or[j] = umax(acc.max_or[j], d2u(fabs(g - w)));
       acc.inf[j] += isinf(g);
       acc.nan[j] += isnan(g);
-      acc.cks[j] += isnan(got) ? Bits<T>::kNaN : Bits<T>::raw(got);
+      acc.cks[j] += bg;
       const double lib = j == 0 ? sin(xd) : j == 1 ? cos(xd) : tan(xd);
       if (isfinite(g) && isfinite(lib)) {
         const double e = fabs(g - lib);
@@ -145,6 +149,7 @@ __global__ void __launch_bounds__(kThreads) k_check(const CheckArgs a) {
   if (lead && v) atomicAdd(reinterpret_cast<unsigned long long*>(&st->field), v);
     FT_MAX(max_ulp[j], acc.max_ulp[j])
     FT_SUM(n_over_tol[j], acc.over[j])
+    FT_SUM(n_bit_mismatch[j], acc.bits[j])
     FT_SUM(n_inf[j], acc.inf[j])
     FT_SUM(n_nan[j], acc.nan[j])
     FT_SUM(n_finite_libm[j], acc.nfin[j])
@@ -167,13 +172,17 @@ __global__ void __launch_bounds__(kThreads) k_check(const CheckArgs a) {
 
 template <typename T>
 cudaError_t check_go(const CheckArgs& a, cudaStream_t s) {
-  const unsigned blocks = persistent_blocks(reinterpret_cast<const void*>(k_check<T>), kThreads, a.n);
+  unsigned blocks = 0;
+  if (const cudaError_t eg = persistent_blocks(reinterpret_cast<const void*>(k_check<T>), kThreads, a.n, &blocks))
+    return eg;
   k_check<T><<<blocks, kThreads, 0, s>>>(a);
   count_launch();
   return cudaGetLastError();
 }
 
 }  // namespace
+
+cudaError_t read_const_table_check(Table* out) { return cudaMemcpyFromSymbol(out, c_table, sizeof(Table)); }
 
 cudaError_t launch_check(ft_dtype dt, const CheckArgs& a, cudaStream_t s) {
   return dt == FT_F32 ? check_go<float>(a, s) : check_go<double>(a, s);

@@ -155,6 +155,16 @@ static __constant__ Table c_table = make_table();
 static __constant__ TaylorCoeffs c_taylor = make_taylor();
 static __constant__ FastConsts c_fast = make_fast_consts();
 
+// Programmatic dependent launch (the launchers set
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel may be
+// scheduled while the previous kernel on its stream drains; it stages its
+// constant tables, then waits here for that kernel's completion (and memory
+// flush) before touching global memory.  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// This block has no more launches to wait for: the next kernel may be scheduled
+// once every block has called it (or exited).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ std::uint64_t d2u(double d) {
   return static_cast<std::uint64_t>(__double_as_longlong(d));
 }
@@ -716,6 +726,177 @@ __device__ __forceinline__ Out3 fast_taylor(double x, int n) {
   return o;
 }
 
+// ======================================================================
+// relaxed_*: f32 inputs at the north-star tolerance (<= 2 ulp of the
+// float-rounded reference, identical segment choice)
+// ======================================================================
+//
+// The reference result for an f32 element is (float)proposed((double)x), so the
+// binary64 value is only needed to ~2^-26 relative: any evaluation within that
+// of the reference's own binary64 result rounds to the same float or to a
+// neighbour (<= 1 ulp).  That frees the reduction and the evaluation:
+//
+//   * one signed reduction for all three functions: m = rint(|x|/pi) from one
+//     FMA with 1.5*2^52 (m in the low word), d = RN(|x| - pi*m) by one FMA.
+//     |d| is the distance from |x| to the nearest multiple of pi, which is
+//     what reduce_sin / reduce_cos / reduce_tan all compute (the quadrant fold
+//     of reduction.hpp:44-52 and the tangent's r > pi/2 fold of :88-89 both
+//     pick the nearest multiple of pi), so red = red_t = |d| and the signs are
+//     bits: sin (d<0) ^ (m odd) ^ (x<0), cos (m odd), tan (d<0) ^ (x<0).
+//     The reference's red differs from |d| only by the rounding of RN(2pi*k)
+//     (resp. RN(pi*k)) -- its other subtractions are exact (Sterbenz) -- so
+//     |red_ref - |d|| <= 2^-38 for |x| < 2^16 (2^-37.9 with d's own rounding);
+//   * the evaluation contracted to FMAs (radicand 2, each numerator and the
+//     tangent denominator 1), every other operation as in the reference.
+//
+// Certification (else the lane takes the bit-exact path, relaxed_slow):
+//   * |x| < 2^16;
+//   * the segment row's high-word bracket (as fast_proposed_core): every
+//     accepted bracket lies >= 5.2e-8 inside its knots, >> 2^-37.9, so the
+//     reference's red is in the same segment;
+//   * the output's relative sensitivity to red is 1/red for sin and tan near
+//     0 (segment 0: b = 0), 1/(pi/2 - red) for cos near pi/2 (c*pi/2 + d = 0
+//     for segment 5), <= ~1000 for tan up to the pole guard and O(1)
+//     elsewhere, so red >= 2^-11 (masks with sin or tan) and red <= pi/2 -
+//     2^-11 (masks with cos) keep it below 2^-37.9 * 2^11 = 2^-26.9;
+//   * the tangent's guard decision |red_t - pi/2| < 1e-3 and its sign are
+//     certain when hi(red) != hi(guard) (the guard sits >= 2.3e-7 inside its
+//     high-word bucket) and hi(red) < hi(pi/2) (row 5's bracket; m's parity
+//     can flip only within ~2^-38 of pi/2).
+// Segment choice is g, the certified row.  tests/test_parity_gpu.py checks all
+// 2^32 float inputs against the bit-exact kernel (<= 1 ulp observed).
+constexpr float kRelaxMaxAbs = 65536.0f;  // 2^16
+constexpr int kHiRelaxLo = 0x3f400000;    // hi(2^-11)
+constexpr int kHiRelaxCos = 0x3ff91ffb;   // hi(pi/2 - 2^-11)
+constexpr int kHiGuard = 0x3ff91de2;      // hi(kFast.guard)
+constexpr double kRintMagic = 0x1.8p52;   // 1.5 * 2^52: RN(v + magic) - magic = rint(v), |v| < 2^51
+
+// The relaxed kernels' rows: coefficients as SmemTable, brackets narrowed by
+// the sensitivity bounds above for the functions MASK evaluates.
+template <unsigned MASK, bool SEG>
+__device__ __forceinline__ void stage_table_relaxed(SmemTable* s) {
+  constexpr bool kLo = (MASK & (kSin | kTan)) != 0 || SEG;
+  constexpr bool kHi = (MASK & kCos) != 0;
+  for (int i = threadIdx.x; i < 8; i += blockDim.x) {
+    const int k = i < 6 ? i : 5;
+    const Coeffs& c = c_table.seg[k];
+    const int klo = i >= 6 ? 0x7fffffff : i == 0 ? (kLo ? kHiRelaxLo : -1) : __double2hiint(c_table.knots[k]);
+    const int khi = i >= 6 ? 0 : i == 5 ? (kHi ? kHiRelaxCos : kHiHalfPi) : __double2hiint(c_table.knots[k + 1]);
+    s->row[i] = SegRow{c.a, c.b, c.c, c.d, c.X, c.Y, c.Z, klo, khi, 0.0, 0.0};
+  }
+}
+
+struct Out3f {
+  float s, c, t;
+  int seg_sc, seg_t;
+};
+
+__device__ __forceinline__ float xor_f(float v, unsigned bits) { return __uint_as_float(__float_as_uint(v) ^ bits); }
+
+template <int SQ, unsigned MASK, bool SEG>
+__device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const SmemTable& tb, int steps, bool* okp) {
+  constexpr bool kS = (MASK & kSin) != 0, kC = (MASK & kCos) != 0, kT = (MASK & kTan) != 0;
+  const FastConsts& K = c_fast;
+  const double a = fabs(static_cast<double>(xf));
+  const double t = __fma_rn(a, K.inv_pi, kRintMagic);
+  const double d = __fma_rn(-K.pi, __dadd_rn(t, -kRintMagic), a);
+  const double red = fabs(d);
+  const unsigned g = static_cast<unsigned>(__double2loint(__fma_rz(red, K.twelve_over_pi, K.two52))) & 7u;
+  const unsigned ra = static_cast<unsigned>(__cvta_generic_to_shared(&tb)) + g * kRowBytes;
+  const int4 zq = lds_i32x4(ra + offsetof(SegRow, Z));
+  const int h = __double2hiint(d) & 0x7fffffff;
+  bool ok = (fabsf(xf) < kRelaxMaxAbs) & (h > zq.z) & (h < zq.w);
+  if constexpr (kT || SEG) ok = ok & (h != kHiGuard);
+  const unsigned modd = static_cast<unsigned>(__double2loint(t)) << 31;  // m odd
+  const unsigned dx = static_cast<unsigned>(__double2hiint(d)) ^ __float_as_uint(xf);
+  Out3f o{0.0f, 0.0f, 0.0f, 0, 0};
+  if constexpr (kS || kC) {
+    double X, Y;
+    lds_f64x2(ra + offsetof(SegRow, X), X, Y);
+    const double rad = __fma_rn(__fma_rn(X, red, Y), red, __hiloint2double(zq.y, zq.x));
+    const double rs = fast_rsqrt<SQ>(rad, steps);
+    if constexpr (kS) {
+      double sa, sb;
+      lds_f64x2(ra + offsetof(SegRow, a), sa, sb);
+      o.s = xor_f(__double2float_rn(__dmul_rn(__fma_rn(sa, red, sb), rs)), (dx ^ modd) & 0x80000000u);
+    }
+    if constexpr (kC) {
+      double sc, sd;
+      lds_f64x2(ra + offsetof(SegRow, c), sc, sd);
+      o.c = xor_f(__double2float_rn(__dmul_rn(__fma_rn(sc, red, sd), rs)), modd);
+    }
+  }
+  const bool guard = h > kHiGuard;
+  if constexpr (kT) {
+    double sa, sb, sc, sd;
+    lds_f64x2(ra + offsetof(SegRow, a), sa, sb);
+    lds_f64x2(ra + offsetof(SegRow, c), sc, sd);
+    const double poly = __fma_rn(sa, red, sb);
+    const double den = __fma_rn(sc, red, sd);
+    double v;
+    if constexpr (SQ == kExact) {
+      v = __ddiv_rn(poly, den);
+    } else {
+      const double r = fast_rsqrt<SQ>(den, steps);
+      v = __dmul_rn(__dmul_rn(poly, r), r);
+    }
+    const float vf = guard ? __int_as_float(0x7f800000) : __double2float_rn(v);
+    o.t = xor_f(vf, dx & 0x80000000u);
+  }
+  if constexpr (SEG) {
+    o.seg_sc = static_cast<int>(g);
+    o.seg_t = guard ? 255 : static_cast<int>(g);
+  }
+  *okp = ok;
+  return o;
+}
+
+// The relaxed kernels' exact path: the bit-exact fused evaluation (its own
+// rows `tbx`, its own mirror fallback), rounded to float.  Out of line.
+template <int SQ, unsigned MASK, bool SEG>
+static __device__ __noinline__ Out3f relaxed_slow(float xf, const SmemTable* tbx, int steps) {
+  const Out3 o = fast_proposed<SQ, MASK, SEG>(static_cast<double>(xf), *tbx, steps);
+  return Out3f{__double2float_rn(o.s), __double2float_rn(o.c), __double2float_rn(o.t), o.seg_sc, o.seg_t};
+}
+
+// Relaxed Taylor sin/cos/tan (NT = 5, 7 or 9 terms): the relaxed reduction and
+// Horner contracted to FMAs.  Brackets: red >= 2^-11 for sin and tan (zero at
+// 0), red <= pi/2 - 2^-11 for cos (the truncated cosine's zero lies within
+// 2.5e-5 of pi/2 for these NT: Taylor-5 cos(pi/2) = -2.47e-5).
+template <int NT, unsigned MASK>
+__device__ __forceinline__ Out3f relaxed_taylor_core(float xf, bool* okp) {
+  constexpr bool kS = (MASK & kSin) != 0, kC = (MASK & kCos) != 0, kT = (MASK & kTan) != 0;
+  const FastConsts& K = c_fast;
+  const double a = fabs(static_cast<double>(xf));
+  const double t = __fma_rn(a, K.inv_pi, kRintMagic);
+  const double d = __fma_rn(-K.pi, __dadd_rn(t, -kRintMagic), a);
+  const double red = fabs(d);
+  const int h = __double2hiint(d) & 0x7fffffff;
+  bool ok = fabsf(xf) < kRelaxMaxAbs;
+  if constexpr (kS || kT) ok = ok & (h > kHiRelaxLo);
+  ok = ok & (h < (kC ? kHiRelaxCos : kHiHalfPi));
+  const unsigned modd = static_cast<unsigned>(__double2loint(t)) << 31;
+  const unsigned dx = static_cast<unsigned>(__double2hiint(d)) ^ __float_as_uint(xf);
+  const double s2 = __dmul_rn(red, red);
+  auto horner = [&](const double* c) {
+    double p = c[NT - 1];
+#pragma unroll
+    for (int k = NT - 2; k >= 0; --k) p = __fma_rn(p, s2, c[k]);
+    return p;
+  };
+  Out3f o{0.0f, 0.0f, 0.0f, 0, 0};
+  if constexpr (kS) o.s = xor_f(__double2float_rn(__dmul_rn(red, horner(c_taylor.sin_c))), (dx ^ modd) & 0x80000000u);
+  if constexpr (kC) o.c = xor_f(__double2float_rn(horner(c_taylor.cos_c)), modd);
+  if constexpr (kT) o.t = xor_f(__double2float_rn(__dmul_rn(red, horner(c_taylor.tan_c))), dx & 0x80000000u);
+  *okp = ok;
+  return o;
+}
+
+template <int NT, unsigned MASK>
+static __device__ __noinline__ Out3f relaxed_taylor_slow(float xf) {
+  const Out3 o = fast_taylor<NT, MASK, true>(static_cast<double>(xf), NT);
+  return Out3f{__double2float_rn(o.s), __double2float_rn(o.c), __double2float_rn(o.t), 0, 0};
+}
 
 #endif  // __CUDACC__
 

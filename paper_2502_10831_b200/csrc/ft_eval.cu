@@ -6,6 +6,8 @@
 // reference returns three vectors from proposed_*_batch, kernels.hpp:84-94).
 // Each thread moves 16 B per access (float4 / double2) with streaming cache
 // hints; the grid is persistent (#SM x resident blocks) and grid-strides.
+#include <cstdlib>
+
 #include "ft_internal.h"
 
 namespace ft {
@@ -38,8 +40,11 @@ constexpr int kMinBlocks = kTmaK1<T> ? 3 : FT_MINB_F32;
 #ifndef FT_MINB_K2_F32
 #define FT_MINB_K2_F32 6
 #endif
-template <typename T>
-constexpr int kMinBlocksK2 = kTmaK2<T> ? 3 : (sizeof(T) == 4 ? FT_MINB_K2_F32 : FT_MINB_F32);
+// The 40-register cap spills in the tan-including instantiations (76 B at NT=0),
+// so those keep K1's 4 blocks/SM.
+template <typename T, unsigned MASK>
+constexpr int kMinBlocksK2 =
+    kTmaK2<T> ? 3 : (sizeof(T) == 4 && (MASK & kTan) == 0 ? FT_MINB_K2_F32 : FT_MINB_F32);
 // Where the exact-path branch sits: 0 one per element; 1 one per vector for
 // tan-only kernels (cfg3 +5%; the fused kernels lose 10% to the extra live
 // registers at the 64-register cap); 2 one per vector everywhere.
@@ -73,6 +78,9 @@ template <>
 __device__ __forceinline__ float to_out<float>(double v) { return __double2float_rn(v); }
 template <>
 __device__ __forceinline__ double to_out<double>(double v) { return v; }
+// Relaxed f32 ops already return floats.
+template <typename T>
+__device__ __forceinline__ T to_out(float v) { return v; }
 
 // TMA bulk store smem -> global (SASS UBLKCP) and its bulk-group completion.
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
@@ -89,7 +97,8 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// The streaming map shared by every evaluation kernel.  `op(double) -> Out3`.
+// The streaming map shared by every evaluation kernel.  `op(T) -> Out3` (or
+// Out3f for the relaxed f32 ops).
 template <typename T, unsigned MASK, bool SEG, class Op, bool TMA = false>
 __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
   using V = Vec<T>;
@@ -114,7 +123,7 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
       T xs[VN], rs[VN], rc[VN], rt[VN];
       std::uint8_t g0[VN], g1[VN];
       V::unpack(xin, xs);
-      auto put = [&](int j, const Out3& o) {
+      auto put = [&](int j, const auto& o) {
         rs[j] = to_out<T>(o.s);
         rc[j] = to_out<T>(o.c);
         rt[j] = to_out<T>(o.t);
@@ -129,25 +138,26 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
         // failing ones exactly.
 #pragma unroll
         for (int j0 = 0; j0 < VN; j0 += G) {
-          Out3 ov[G];
+          using OutT = decltype(op.core(xs[0], nullptr));
+          OutT ov[G];
           bool okv[G];
           bool all = true;
 #pragma unroll
           for (int j = 0; j < G; ++j) {
-            ov[j] = op.core(static_cast<double>(xs[j0 + j]), &okv[j]);
+            ov[j] = op.core(xs[j0 + j], &okv[j]);
             all = all && okv[j];
           }
           if (!all) {
 #pragma unroll
             for (int j = 0; j < G; ++j)
-              if (!okv[j]) ov[j] = op.slow(static_cast<double>(xs[j0 + j]));
+              if (!okv[j]) ov[j] = op.slow(xs[j0 + j]);
           }
 #pragma unroll
           for (int j = 0; j < G; ++j) put(j0 + j, ov[j]);
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < VN; ++j) put(j, op(static_cast<double>(xs[j])));
+        for (int j = 0; j < VN; ++j) put(j, op(xs[j]));
       }
       res[0] = V::pack(rs);
       res[1] = V::pack(rc);
@@ -226,8 +236,9 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
 
     done = nv * VN;
   }
+  pdl_trigger();
   for (unsigned i = done + tid; i < n; i += stride) {
-    const Out3 o = op(static_cast<double>(x[i]));
+    const auto o = op(x[i]);
     if constexpr ((MASK & kSin) != 0) o0[i] = to_out<T>(o.s);
     if constexpr ((MASK & kCos) != 0) o1[i] = to_out<T>(o.c);
     if constexpr ((MASK & kTan) != 0) o2[i] = to_out<T>(o.t);
@@ -264,6 +275,44 @@ struct TaylorOp {
   __device__ __forceinline__ Out3 operator()(double x) const { return fast_taylor<NT, MASK, CERT>(x, n); }
 };
 
+// Relaxed f32 proposed path (ft_core.cuh: relaxed_proposed_core): certified
+// lanes within 2 ulp of the reference, the rest redone bit-exactly.
+#ifndef FT_RELAX_GROUP
+#define FT_RELAX_GROUP 1  // elements per exact-path branch in the relaxed kernels
+#endif
+template <int SQ, unsigned MASK, bool SEG>
+struct RelaxedOp {
+  template <typename T>
+  static constexpr int kGroup = FT_RELAX_GROUP;
+  const SmemTable* tb;   // relaxed rows
+  const SmemTable* tbx;  // bit-exact rows (fallback)
+  int steps;
+  __device__ __forceinline__ Out3f operator()(float x) const {
+    bool ok;
+    Out3f o = relaxed_proposed_core<SQ, MASK, SEG>(x, *tb, steps, &ok);
+    if (!ok) o = relaxed_slow<SQ, MASK, SEG>(x, tbx, steps);  // rare
+    return o;
+  }
+  __device__ __forceinline__ Out3f core(float x, bool* ok) const {
+    return relaxed_proposed_core<SQ, MASK, SEG>(x, *tb, steps, ok);
+  }
+  __device__ __forceinline__ Out3f slow(float x) const { return relaxed_slow<SQ, MASK, SEG>(x, tbx, steps); }
+};
+
+template <int NT, unsigned MASK>
+struct RelaxedTaylorOp {
+  template <typename T>
+  static constexpr int kGroup = FT_RELAX_GROUP;
+  __device__ __forceinline__ Out3f operator()(float x) const {
+    bool ok;
+    Out3f o = relaxed_taylor_core<NT, MASK>(x, &ok);
+    if (!ok) o = relaxed_taylor_slow<NT, MASK>(x);  // rare
+    return o;
+  }
+  __device__ __forceinline__ Out3f core(float x, bool* ok) const { return relaxed_taylor_core<NT, MASK>(x, ok); }
+  __device__ __forceinline__ Out3f slow(float x) const { return relaxed_taylor_slow<NT, MASK>(x); }
+};
+
 // Device restatement: each function evaluated separately, exactly as the
 // reference scalar code does (kernels.hpp:46-67 / SPEC.md:224-247).
 template <unsigned MASK>
@@ -294,15 +343,48 @@ template <typename T, int SQ, unsigned MASK, bool SEG>
 __global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_proposed(const EvalArgs a) {
   __shared__ SmemTable tb;
   stage_table(&tb);
+  pdl_wait();
   __syncthreads();
   stream_map<T, MASK, SEG, ProposedOp<SQ, MASK, SEG>, kTmaK1<T>>(a, ProposedOp<SQ, MASK, SEG>{&tb, a.steps});
 }
 
 // ---------------- K2 ----------------
 template <typename T, int NT, unsigned MASK>
-__global__ void __launch_bounds__(kThreads, kMinBlocksK2<T>) k_taylor(const EvalArgs a) {
+__global__ void __launch_bounds__(kThreads, (kMinBlocksK2<T, MASK>)) k_taylor(const EvalArgs a) {
   using Op = TaylorOp<NT, MASK, sizeof(T) == 4>;  // certify-or-redo for the instruction-bound f32 kernels
+  pdl_wait();
   stream_map<T, MASK, false, Op, kTmaK2<T>>(a, Op{a.steps});
+}
+
+// ---------------- relaxed f32 K1 / K2 ----------------
+#ifndef FT_MINB_RELAX
+#define FT_MINB_RELAX 4
+#endif
+#ifndef FT_TMA_RELAX
+#define FT_TMA_RELAX 0
+#endif
+// Relaxed Taylor f32: 5 blocks/SM (48 registers) measured 496 vs 462 Gelem/s
+// at 4 (cfg4 f32, r02c); tan-including masks keep 4.
+#ifndef FT_MINB_RELAX_TAYLOR
+#define FT_MINB_RELAX_TAYLOR 5
+#endif
+template <int SQ, unsigned MASK, bool SEG>
+__global__ void __launch_bounds__(kThreads, FT_MINB_RELAX) k_proposed_relaxed(const EvalArgs a) {
+  __shared__ SmemTable tb[2];
+  stage_table_relaxed<MASK, SEG>(&tb[0]);
+  stage_table(&tb[1]);
+  pdl_wait();
+  __syncthreads();
+  using Op = RelaxedOp<SQ, MASK, SEG>;
+  stream_map<float, MASK, SEG, Op, FT_TMA_RELAX != 0>(a, Op{&tb[0], &tb[1], a.steps});
+}
+
+template <int NT, unsigned MASK>
+__global__ void __launch_bounds__(kThreads, (MASK & kTan) ? FT_MINB_RELAX : FT_MINB_RELAX_TAYLOR)
+    k_taylor_relaxed(const EvalArgs a) {
+  using Op = RelaxedTaylorOp<NT, MASK>;
+  pdl_wait();
+  stream_map<float, MASK, false, Op, FT_TMA_RELAX != 0>(a, Op{});
 }
 
 // ---------------- device restatement ----------------
@@ -311,12 +393,39 @@ __global__ void __launch_bounds__(kThreads) k_mirror(const EvalArgs a, int kind,
   stream_map<T, MASK, true>(a, MirrorOp<MASK>{kind, method, a.steps, a.steps});
 }
 
+// Grid waves of resident blocks: the relaxed f32 kernels run one wave (they
+// stage two row tables per block, and with PDL the next launch's staging hides
+// under this one's tail: cfg1 306 vs 294 Gelem/s at 4 waves); the others use
+// persistent_blocks' default (4, tail backfill).
+#ifndef FT_RELAX_WAVES
+#define FT_RELAX_WAVES 1
+#endif
+// FT_PDL=0 in the environment launches without programmatic dependent launch.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FT_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class K>
-cudaError_t go(K kernel, const EvalArgs& a, cudaStream_t s, int threads = kThreads) {
-  const unsigned blocks = persistent_blocks(reinterpret_cast<const void*>(kernel), threads, a.n);
-  kernel<<<blocks, threads, 0, s>>>(a);
+cudaError_t go(K kernel, const EvalArgs& a, cudaStream_t s, int waves = 0) {
+  unsigned blocks = 0;
+  if (const cudaError_t eg = persistent_blocks(reinterpret_cast<const void*>(kernel), kThreads, a.n, &blocks, waves))
+    return eg;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, a);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 #define FT_MASK_SWITCH(MASK_VAR, EXPR_OF_M)   \
@@ -341,10 +450,31 @@ cudaError_t taylor_t(unsigned mask, const EvalArgs& a, cudaStream_t s) {
   FT_MASK_SWITCH(mask, (go(k_taylor<T, NT, M>, a, s)))
 }
 
+template <int SQ, bool SEG>
+cudaError_t relaxed_t(unsigned mask, const EvalArgs& a, cudaStream_t s) {
+  FT_MASK_SWITCH(mask, (go(k_proposed_relaxed<SQ, M, SEG>, a, s, FT_RELAX_WAVES)))
+}
+
+template <int NT>
+cudaError_t taylor_relaxed_t(unsigned mask, const EvalArgs& a, cudaStream_t s) {
+  FT_MASK_SWITCH(mask, (go(k_taylor_relaxed<NT, M>, a, s, FT_RELAX_WAVES)))
+}
+
+template <bool SEG>
+cudaError_t relaxed_dt(unsigned mask, int sq, const EvalArgs& a, cudaStream_t s) {
+  switch (sq) {
+    case kExact: return relaxed_t<kExact, SEG>(mask, a, s);
+    case kFisr1: return relaxed_t<kFisr1, SEG>(mask, a, s);
+    case kFisr2: return relaxed_t<kFisr2, SEG>(mask, a, s);
+    default: return relaxed_t<kFisrN, SEG>(mask, a, s);
+  }
+}
+
 template <typename T, unsigned M>
 cudaError_t mirror_go(const EvalArgs& a, int kind, int method, cudaStream_t s) {
-  const unsigned blocks =
-      persistent_blocks(reinterpret_cast<const void*>(k_mirror<T, M>), kThreads, a.n);
+  unsigned blocks = 0;
+  if (const cudaError_t eg = persistent_blocks(reinterpret_cast<const void*>(k_mirror<T, M>), kThreads, a.n, &blocks))
+    return eg;
   k_mirror<T, M><<<blocks, kThreads, 0, s>>>(a, kind, method);
   count_launch();
   return cudaGetLastError();
@@ -375,6 +505,16 @@ cudaError_t proposed_dt(unsigned mask, int sq, bool seg, const EvalArgs& a, cuda
 
 template <typename T>
 cudaError_t taylor_dt(unsigned mask, int n_terms, const EvalArgs& a, cudaStream_t s) {
+  if constexpr (sizeof(T) == 4) {
+    if (f32_policy() == FT_F32_ULP2) {
+      switch (n_terms) {
+        case 5: return taylor_relaxed_t<5>(mask, a, s);
+        case 7: return taylor_relaxed_t<7>(mask, a, s);
+        case 9: return taylor_relaxed_t<9>(mask, a, s);
+        default: break;  // other term counts: the truncated cosine's zero is not near pi/2
+      }
+    }
+  }
   switch (n_terms) {
     case 5: return taylor_t<T, 5>(mask, a, s);
     case 7: return taylor_t<T, 7>(mask, a, s);
@@ -405,11 +545,42 @@ cudaError_t chunked(ft_dtype dt, const EvalArgs& a, F&& launch_one) {
   return cudaSuccess;
 }
 
+// The shared-memory rows exactly as the kernels stage them, copied out
+// (kind 0: bit-exact K1 rows; kind 1..7: relaxed f32 rows for that mask).
+__global__ void k_dump_rows(int kind, SmemTable* out) {
+  __shared__ SmemTable tb;
+  switch (kind) {
+    case 1: stage_table_relaxed<1, false>(&tb); break;
+    case 2: stage_table_relaxed<2, false>(&tb); break;
+    case 3: stage_table_relaxed<3, false>(&tb); break;
+    case 4: stage_table_relaxed<4, false>(&tb); break;
+    case 5: stage_table_relaxed<5, false>(&tb); break;
+    case 6: stage_table_relaxed<6, false>(&tb); break;
+    case 7: stage_table_relaxed<7, false>(&tb); break;
+    default: stage_table(&tb); break;
+  }
+  __syncthreads();
+  const int4* src = reinterpret_cast<const int4*>(&tb);
+  int4* dst = reinterpret_cast<int4*>(out);
+  for (unsigned i = threadIdx.x; i < sizeof(SmemTable) / 16; i += blockDim.x) dst[i] = src[i];
+}
+
 }  // namespace
+
+cudaError_t read_const_table_eval(Table* out) { return cudaMemcpyFromSymbol(out, c_table, sizeof(Table)); }
+
+cudaError_t launch_dump_rows(int kind, void* out640, cudaStream_t s) {
+  static_assert(sizeof(SmemTable) == 640, "8 rows x 80 bytes");
+  k_dump_rows<<<1, 32, 0, s>>>(kind, static_cast<SmemTable*>(out640));
+  count_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_proposed(ft_dtype dt, unsigned mask, int sq, bool seg, const EvalArgs& a,
                             cudaStream_t s) {
+  const bool relaxed = dt == FT_F32 && f32_policy() == FT_F32_ULP2;
   return chunked(dt, a, [&](const EvalArgs& b) {
+    if (relaxed) return seg ? relaxed_dt<true>(mask, sq, b, s) : relaxed_dt<false>(mask, sq, b, s);
     return dt == FT_F32 ? proposed_dt<float>(mask, sq, seg, b, s) : proposed_dt<double>(mask, sq, seg, b, s);
   });
 }

@@ -75,13 +75,14 @@ __global__ void __launch_bounds__(kThreads) k_fill(uint4* __restrict__ buf, std:
 template <typename T>
 cudaError_t gen_go(int dist, double lo, double hi, std::uint64_t seed, std::uint64_t offset,
                    std::size_t n, void* x, cudaStream_t s) {
+  unsigned blocks = 0;
   if (dist == FT_DIST_UNIFORM) {
-    const unsigned blocks =
-        persistent_blocks(reinterpret_cast<const void*>(k_gen_uniform<T>), kThreads, n);
+    if (const cudaError_t e = persistent_blocks(reinterpret_cast<const void*>(k_gen_uniform<T>), kThreads, n, &blocks))
+      return e;
     k_gen_uniform<T><<<blocks, kThreads, 0, s>>>(static_cast<T*>(x), n, lo, hi - lo, seed, offset);
   } else {
-    const unsigned blocks =
-        persistent_blocks(reinterpret_cast<const void*>(k_gen_tan_stress<T>), kThreads, n);
+    if (const cudaError_t e = persistent_blocks(reinterpret_cast<const void*>(k_gen_tan_stress<T>), kThreads, n, &blocks))
+      return e;
     k_gen_tan_stress<T><<<blocks, kThreads, 0, s>>>(static_cast<T*>(x), n,
                                                     static_cast<std::int64_t>(lo),
                                                     static_cast<std::int64_t>(hi), seed, offset);
@@ -98,9 +99,13 @@ cudaError_t launch_gen(ft_dtype dt, int dist, double lo, double hi, std::uint64_
                       : gen_go<double>(dist, lo, hi, seed, offset, n, x, s);
 }
 
+cudaError_t read_const_table_gen(Table* out) { return cudaMemcpyFromSymbol(out, c_table, sizeof(Table)); }
+
 cudaError_t launch_fill(void* buf, std::size_t bytes, unsigned v, cudaStream_t s) {
   const std::size_t n16 = bytes / 16;
-  const unsigned blocks = persistent_blocks(reinterpret_cast<const void*>(k_fill), kThreads, n16);
+  unsigned blocks = 0;
+  if (const cudaError_t e = persistent_blocks(reinterpret_cast<const void*>(k_fill), kThreads, n16, &blocks))
+    return e;
   k_fill<<<blocks, kThreads, 0, s>>>(static_cast<uint4*>(buf), n16, v);
   count_launch();
   return cudaGetLastError();

@@ -47,9 +47,22 @@ cudaError_t launch_gen(ft_dtype dt, int dist, double lo, double hi, std::uint64_
                        std::uint64_t offset, std::size_t n, void* x, cudaStream_t s);
 cudaError_t launch_fill(void* buf, std::size_t bytes, unsigned v, cudaStream_t s);
 
-// Grid sizing: a persistent grid of (#SM x resident blocks) for `fn`, capped
-// by the work available.
-unsigned persistent_blocks(const void* fn, int threads, std::size_t work_items);
+// Grid sizing: waves x (#SM x resident blocks of `fn` at `threads` per block),
+// capped by the work available (work_items / threads blocks).  `waves` > 0
+// overrides the default (4).  Fails (and sets no grid) if the device or
+// occupancy queries fail.
+cudaError_t persistent_blocks(const void* fn, int threads, std::size_t work_items, unsigned* blocks,
+                              int waves = 0);
+// Read-back of the device-resident tables (ft_device_const_table /
+// ft_device_rows): the __constant__ segment table of each translation unit
+// that evaluates the path, and the shared-memory rows K1 stages.
+cudaError_t read_const_table_eval(Table* out);
+cudaError_t read_const_table_check(Table* out);
+cudaError_t read_const_table_gen(Table* out);
+cudaError_t launch_dump_rows(int kind, void* out640, cudaStream_t s);
+
+// Process-wide f32 policy (ft_set_f32_policy): FT_F32_ULP2 or FT_F32_BITWISE.
+int f32_policy();
 void count_launch();
 
 }  // namespace ft

@@ -4,7 +4,9 @@
 // reference headers are absent (the stand-in SqrtMode is used); compiled
 // (-fsyntax-only) against the real reference headers by tests/test_cpp_header.py.
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numbers>
 #include <vector>
@@ -46,11 +48,24 @@ int main() {
   EXPECT(std::memcmp(f.sin.data(), s.data(), xs.size() * 8) == 0);
   EXPECT(std::memcmp(f.tan.data(), t.data(), xs.size() * 8) == 0);
 
-  // f32 overload == (float) of the f64 result
+  // f32 overload: bitwise policy == (float) of the f64 result; default policy
+  // within 2 ulp of it
   std::vector<float> xf(xs.begin(), xs.end());
-  auto sf = g::proposed_sin_batch(std::span<const float>(xf));
+  for (int k = 0; k < 2000; ++k) xf.push_back(-300.0f + 0.3f * static_cast<float>(k));
   auto sd = g::proposed_sin_batch(std::vector<double>(xf.begin(), xf.end()));
-  for (std::size_t i = 0; i < xf.size(); ++i) EXPECT(sf[i] == static_cast<float>(sd[i]));
+  EXPECT(g::f32_policy() == g::F32Policy::ulp2);
+  auto sf = g::proposed_sin_batch(std::span<const float>(xf));
+  for (std::size_t i = 0; i < xf.size(); ++i) {
+    const float want = static_cast<float>(sd[i]);
+    std::int32_t a, b;
+    std::memcpy(&a, &sf[i], 4);
+    std::memcpy(&b, &want, 4);
+    EXPECT(std::abs(static_cast<long long>(a) - b) <= 2 && (a < 0) == (b < 0));
+  }
+  g::set_f32_policy(g::F32Policy::bitwise);
+  auto sb = g::proposed_sin_batch(std::span<const float>(xf));
+  for (std::size_t i = 0; i < xf.size(); ++i) EXPECT(sb[i] == static_cast<float>(sd[i]));
+  g::set_f32_policy(g::F32Policy::ulp2);
 
   // larger batch: element i == element i of a one-element batch (kernels.hpp:82-83)
   std::vector<double> big(100003);

@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol(ft):
     nm = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
     for s in syms:
         assert re.search(rf"\bT {s}\b", nm), s
-    assert L.ft_abi_version() == 1
+    assert L.ft_abi_version() == 2
 
 
 def test_device_table_is_reference_table(ft, golden):
@@ -79,7 +79,8 @@ def test_hiword_constants(ft):
     th = ft.thresholds()
     hi = lambda v: int(np.float64(v).view(np.uint64) >> np.uint64(32))  # noqa: E731
     assert const == {"kHiHalfPi": hi(th[0]), "kHiPiQ": hi(th[1]), "kHiThreeHalfPi": hi(th[2]),
-                     "kHiRow0Lo": hi(2.0 ** -17)}
+                     "kHiRow0Lo": hi(2.0 ** -17), "kHiGuard": hi(th[3]), "kHiRelaxLo": hi(2.0 ** -11),
+                     "kHiRelaxCos": hi(0.5 * math.pi - 2.0 ** -11)}
     assert hi(th[0]) == hi(0.5 * math.pi)  # tan fold threshold (r > pi/2) shares it
     P = math.pi
     bottom = lambda t: (np.uint64(hi(t)) << np.uint64(32)).view(np.float64)  # noqa: E731
@@ -260,3 +261,55 @@ def test_host_device_setting_roundtrip(ft):
     ft.set_host_devices(0)
     assert ft.get_host_devices() == 0
     ft.set_host_devices(1)
+
+
+def _rn_fma_reduce(a: float) -> tuple[float, int]:
+    """The relaxed f32 reduction (ft_core.cuh relaxed_proposed_core) in exact
+    rational arithmetic: m = rint(a * RN(1/pi)) (one FMA with 1.5*2^52),
+    d = RN(a - pi*m) (one FMA)."""
+    from fractions import Fraction as F
+
+    inv_pi = F(2.0 * (1.0 / (2.0 * math.pi)))  # RN(1/pi) = 2 RN(1/2pi), as in kFast.inv_pi
+    t = float(F(a) * inv_pi + F(float.fromhex("0x1.8p52")))  # RN of the exact FMA result
+    m = int(t - float.fromhex("0x1.8p52"))
+    d = float(F(a) - F(math.pi) * m)
+    return d, m
+
+
+def test_relaxed_reduction_error_bound():
+    """DESIGN.md section 3 / ft_core.cuh relaxed_*: for |x| < 2^16 the one-FMA
+    signed reduction |d| differs from the reference's red (reduce_sin, reduce_tan)
+    by <= 2^-37.9, and the sign bits it implies equal the reference's signs
+    wherever the relaxed brackets accept the lane (2^-11 <= |d| < hi(pi/2))."""
+    from oracle import oracle as O
+
+    L = O.port()
+    rng = np.random.default_rng(5)
+    k = rng.integers(1, 20860, 4000)  # multiples of pi/2 up to 2^15
+    xs = np.concatenate([rng.uniform(0, 65536, 6000), rng.uniform(0, 8, 2000),
+                         k * (math.pi / 2) + rng.uniform(-1e-3, 1e-3, k.size)]).astype(np.float32)
+    worst = 0.0
+    for xf in xs:
+        a = float(xf)
+        if a == 0.0:
+            continue
+        d, m = _rn_fma_reduce(a)
+        for which in (0, 2):
+            red, sign = C.c_double(), C.c_double()
+            getattr(L, "ora_reduce_sin" if which == 0 else "ora_reduce_tan")(a, C.byref(red), C.byref(sign))
+            worst = max(worst, abs(abs(d) - red.value))
+            if 2.0 ** -11 <= abs(d) < 0.5 * math.pi - 3.1e-7:
+                want = (-1.0 if d < 0 else 1.0) * (-1.0 if (which == 0 and m % 2) else 1.0)
+                assert sign.value == want, (a, which)
+    assert worst <= 2.0 ** -37.9, worst
+
+
+def test_relaxed_guard_bucket_margin():
+    """The relaxed kernels decide the pole guard from hi(red) and reject
+    hi(red) == hi(guard): the guard must sit well inside its high-word bucket
+    (>> the 2^-37.9 reduction error), so the decision is the reference's."""
+    g = float.fromhex("0x1.91de2c0cf70aep+0")
+    b = int(np.float64(g).view(np.uint64))
+    lo = (np.uint64(b >> 32 << 32)).view(np.float64)
+    hi = (np.uint64((b >> 32 << 32) | 0xFFFFFFFF)).view(np.float64)
+    assert g - lo > 2.3e-7 and hi - g > 2.3e-7

@@ -1,0 +1,148 @@
+"""The default f32 policy (FT_F32_ULP2) and the bit-exact one over EVERY float.
+
+The reference is double-only; for f32 inputs its result is
+(float)proposed_*((double)x) (R:proj/include/fasttrig/kernels.hpp:46-67).  The
+f32 domain has 2^32 inputs, so parity here is proven, not sampled:
+
+* the production relaxed kernels (ft_core.cuh relaxed_*) against the production
+  bit-exact kernels, all 2^32 bit patterns, through K3 with the bit-exact outputs
+  as the oracle arrays: <= 2 ulp (the north-star tolerance; <= 1 observed) and
+  identical segment choices (SEG instantiations compared element for element);
+* the production bit-exact kernels against the device restatement (K3, 0 ulp);
+* both, for fisr(1) and all three outputs, against the UNMODIFIED reference
+  library on the host (oracle/_ref, all host threads): values and segments.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+MODES = {"fisr1": (1, 1), "exact": (0, 0)}
+CHUNK = 1 << 28
+ALL = 1 << 32
+
+
+def chunk_bits(start: int, n: int):
+    """float32 CUDA tensor whose bit patterns are start .. start+n-1."""
+    s = start - (1 << 32) if start >= (1 << 31) else start
+    b = torch.arange(n, dtype=torch.int32, device="cuda")
+    b.add_(s)
+    return b.view(torch.float32)
+
+
+def _stats_buf():
+    return torch.zeros(312, dtype=torch.uint8, device="cuda")
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("mask", [7, 3, 4, 1, 2, 5, 6])
+def test_every_float_relaxed_within_2ulp_same_segments(ft, mask, mode):
+    if mode == "exact" and mask not in (7, 3, 4):
+        pytest.skip("exact mode: masks 7, 3, 4")
+    sm = ft.SqrtMode(*MODES[mode])
+    buf = _stats_buf()
+    max_ulp, over, seg_mm, checked = [0, 0, 0], [0, 0, 0], [0, 0], 0
+    for start in range(0, ALL, CHUNK):
+        x = chunk_bits(start, CHUNK)
+        with ft.f32_policy("ulp2"):
+            got = ft.proposed_eval(x, mask, sm)
+        with ft.f32_policy("bitwise"):
+            ref = ft.proposed_eval(x, mask, sm)
+        st = ft.parity_reduce(x, got, mask, mode=sm, refs=ref, ulp_tol=2, stats_buf=buf)
+        checked += st["n_checked"]
+        for j in range(3):
+            max_ulp[j] = max(max_ulp[j], st["max_ulp"][j])
+            over[j] += st["n_over_tol"][j]
+        del got, ref
+        with ft.f32_policy("ulp2"):
+            gs = ft.proposed_eval(x, mask, sm, seg=True)
+        with ft.f32_policy("bitwise"):
+            rs = ft.proposed_eval(x, mask, sm, seg=True)
+        seg_mm[0] += int((gs["seg_sc"] != rs["seg_sc"]).sum())
+        seg_mm[1] += int((gs["seg_t"] != rs["seg_t"]).sum())
+        del gs, rs
+    assert checked == ALL
+    assert over == [0, 0, 0] and max(max_ulp) <= 2, max_ulp
+    assert seg_mm == [0, 0]
+
+
+@pytest.mark.parametrize("mask", [3, 7])
+@pytest.mark.parametrize("nt", [5, 7, 9])
+def test_every_float_relaxed_taylor_within_2ulp(ft, nt, mask):
+    buf = _stats_buf()
+    max_ulp, over = [0, 0, 0], [0, 0, 0]
+    for start in range(0, ALL, CHUNK):
+        x = chunk_bits(start, CHUNK)
+        with ft.f32_policy("ulp2"):
+            got = ft.taylor_eval(x, nt, mask)
+        with ft.f32_policy("bitwise"):
+            ref = ft.taylor_eval(x, nt, mask)
+        st = ft.parity_reduce(x, got, mask, kind=1, n_terms=nt, refs=ref, ulp_tol=2, stats_buf=buf)
+        for j in range(3):
+            max_ulp[j] = max(max_ulp[j], st["max_ulp"][j])
+            over[j] += st["n_over_tol"][j]
+    assert over == [0, 0, 0] and max(max_ulp) <= 2, max_ulp
+
+
+@pytest.mark.parametrize("case", ["fisr1-7", "fisr1-3", "fisr1-4", "exact-7", "taylor5-3"])
+def test_every_float_bitwise_production_vs_restatement(ft, case):
+    """The production (non-SEG) bit-exact kernels against the device restatement
+    (itself pinned to the CPU oracle): 0 ulp and identical bits on every float."""
+    kind, mask = case.split("-")
+    mask = int(mask)
+    buf = _stats_buf()
+    tot = {"max_ulp": [0, 0, 0], "bits": [0, 0, 0]}
+    for start in range(0, ALL, CHUNK):
+        x = chunk_bits(start, CHUNK)
+        with ft.f32_policy("bitwise"):
+            if kind == "taylor5":
+                out = ft.taylor_eval(x, 5, mask)
+                st = ft.parity_reduce(x, out, mask, kind=1, n_terms=5, ulp_tol=0, stats_buf=buf)
+            else:
+                sm = ft.SqrtMode(*MODES[kind])
+                out = ft.proposed_eval(x, mask, sm)
+                st = ft.parity_reduce(x, out, mask, mode=sm, ulp_tol=0, stats_buf=buf)
+        for j in range(3):
+            tot["max_ulp"][j] = max(tot["max_ulp"][j], st["max_ulp"][j])
+            tot["bits"][j] += st["n_bit_mismatch"][j]
+    assert tot["max_ulp"] == [0, 0, 0] and tot["bits"] == [0, 0, 0], tot
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("policy", ["bitwise", "ulp2"])
+def test_every_float_vs_reference_library(ft, policy):
+    """fisr(1), all three outputs and both segment choices, every float, against
+    the unmodified reference compiled on the host (oracle/_ref)."""
+    n = 1 << 26
+    hs = {f: torch.empty(n, dtype=torch.float32, pin_memory=True) for f in ("sin", "cos", "tan")}
+    hg = {f: torch.empty(n, dtype=torch.uint8, pin_memory=True) for f in ("seg_sc", "seg_t")}
+    tot = {"max_ulp": [0, 0, 0], "n_bit_mismatch": [0, 0, 0], "n_over_2ulp": [0, 0, 0], "seg_mismatch": [0, 0]}
+    for start in range(0, ALL, n):
+        x = chunk_bits(start, n)
+        with ft.f32_policy(policy):
+            out = ft.proposed_eval(x, 7)
+            seg = ft.proposed_eval(x, 7, seg=True)
+        for f in hs:
+            hs[f].copy_(out[f])
+        for f in hg:
+            hg[f].copy_(seg[f])
+        torch.cuda.synchronize()
+        r = O.ref_check_f32_range(start, {**{f: hs[f].numpy() for f in hs}, **{f: hg[f].numpy() for f in hg}})
+        for j in range(3):
+            tot["max_ulp"][j] = max(tot["max_ulp"][j], r["max_ulp"][j])
+            tot["n_bit_mismatch"][j] += r["n_bit_mismatch"][j]
+            tot["n_over_2ulp"][j] += r["n_over_2ulp"][j]
+        for j in range(2):
+            tot["seg_mismatch"][j] += r["seg_mismatch"][j]
+    print(policy, tot)
+    assert tot["seg_mismatch"] == [0, 0]
+    assert tot["n_over_2ulp"] == [0, 0, 0]
+    if policy == "bitwise":
+        assert tot["n_bit_mismatch"] == [0, 0, 0] and tot["max_ulp"] == [0, 0, 0]
+    else:
+        assert max(tot["max_ulp"]) <= 2

@@ -2,7 +2,7 @@
 
     python tools/ncu_summarize.py r01g [--update-json]
 
-For each gpurun_out/<tag>_{k1_cfg2,k1_cfg1,k2_cfg4f32}.ncu-rep writes
+For each gpurun_out/<tag>_<kernel>_<cfgN>.ncu-rep (e.g. r02d_k1r_cfg1) writes
 profiles/<tag>_<name>_ncu_summary.txt (the metrics quoted in DESIGN.md /
 profiles/README.md, plus the PC-sampling stall reasons) and
 profiles/<tag>_<name>_ncu_details.csv (the details page).  --update-json
@@ -17,7 +17,21 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-CAPTURES = {"k1_cfg2": ("cfg2", 1 << 28), "k1_cfg1": ("cfg1", 1 << 24), "k2_cfg4f32": ("cfg4_f32", 1 << 28)}
+# capture-name suffix -> (workload, elements per launch of tools/run_kernel.py)
+WORKLOADS = {"cfg1": ("cfg1", 1 << 24), "cfg2": ("cfg2", 1 << 28), "cfg3": ("cfg3", 1 << 26),
+             "cfg4f32": ("cfg4_f32", 1 << 28), "cfg4f64": ("cfg4_f64", 1 << 28), "cfg5": ("cfg5", 1 << 30)}
+
+
+def captures(tag):
+    """{name: (workload, n)} for every gpurun_out/<tag>_<name>.ncu-rep."""
+    import glob
+    out = {}
+    for f in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", f"{tag}_*.ncu-rep"))):
+        name = os.path.basename(f)[len(tag) + 1:-len(".ncu-rep")]
+        wl = WORKLOADS.get(name.rsplit("_", 1)[-1])
+        if wl:
+            out[name] = wl
+    return out
 METRICS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
@@ -59,7 +73,7 @@ def main():
     update = "--update-json" in sys.argv
     js_path = os.path.join(ROOT, "profiles", "ncu_k1_summary.json")
     js = json.load(open(js_path)) if os.path.exists(js_path) else {}
-    for name, (wl, n) in CAPTURES.items():
+    for name, (wl, n) in captures(tag).items():
         rep = os.path.join(ROOT, "gpurun_out", f"{tag}_{name}.ncu-rep")
         if not os.path.exists(rep):
             print("missing", rep)
@@ -92,10 +106,6 @@ def main():
             if fp64:
                 per = round(fp64 * 32 / n, 2)
                 js.setdefault("fp64_pipe_instr_per_elem", {})[wl] = per
-                if wl == "cfg2":
-                    js["fp64_pipe_instr_per_elem"]["cfg5"] = per
-                if wl == "cfg4_f32":
-                    js["fp64_pipe_instr_per_elem"]["cfg4_f64"] = per
             js["source"] = (f"ncu --set full --clock-control none, one launch per workload "
                             f"(profiles/{tag}_*_ncu_summary.txt)")
     if update:
