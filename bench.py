@@ -1,26 +1,39 @@
 """Benchmark of the B200 batched piecewise sin/cos/tan path (arXiv 2502.10831).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2] [--configs auto|none|cfg1,cfg3,...] [--elements N]
+                    [--backend nccl|gloo] [--f32-policy ulp2|bitwise]
+                    [--no-e2e] [--no-cpu] [--e2e-elements N] [--e2e-steps S]
 
-Workload (N=1): BASELINE.json configs[1] -- f64 x, 2^28 elements uniform in
+Headline (N=1): BASELINE.json configs[1] -- f64 x, 2^28 elements uniform in
 [-1000pi, 1000pi], fused proposed sin+cos+tan (three output arrays), default
 SqrtMode (fisr, 1 Newton step).  Under torchrun each rank owns a contiguous
 2^28-element shard of one global array (global index = generator counter):
 per-GPU work is fixed, so "scaling": "weak".  No element data moves between
-GPUs; after the timed region each rank runs the K3 parity/error reduction and
-NCCL all-reduces the 64-byte statistics (max / sum), the only collective.
+GPUs; after each timed region every rank runs the K3 parity/error reduction and
+the ranks all-reduce the 312-byte statistics (max / sum), the only collective.
 
-One step = one K1 launch over the shard (inputs already resident in HBM).
-Inputs + outputs are 8 GiB per GPU, far above the 126 MB L2, so no flush is
-needed between steps.  Timing: CUDA events on the launching stream, barrier +
-synchronize on both sides, max over ranks.
+The same run also times every other BASELINE config and reports it under
+`configs` (value, ms, roofline, FP64 roof, clocks, K3 accuracy each): cfg1, cfg3,
+cfg4_f32, cfg4_f64 weak-scaled per GPU, and cfg5 -- the fixed 2^33-element f32
+array -- strong-scaled (N=1: all 2^33 elements on one GPU; N>1: 2^33/N each).
 
-`e2e` is the same metric through the public host-pointer C-ABI call
-(ft_proposed_batch_host) with pinned host buffers: every step copies x in and
-sin/cos/tan out (2^26 elements per rank per step by default, so N ranks pin
-N x 2 GiB of host memory, not N x 8 GiB; the rate is PCIe-bound either way).  `cpu_baseline` (rank 0, N=1) and `--impl reference` time the
-reference's own CPU implementation (oracle/_ref: the unmodified reference
-headers, all host threads) on a bounded sample of the same workload.
+One step = one K1/K2 launch sequence over the shard (inputs already resident in
+HBM).  L2: the headline's x + outputs are 8 GiB per GPU (>> 126 MB L2), no
+flush; configs whose input is smaller than L2 (cfg1) are timed step by step
+with a 2x-L2 flush between steps (outside the timed pairs).  Timing: CUDA
+events on the launching stream, barrier + synchronize on both sides, max over
+ranks.
+
+`e2e` is the headline metric through the public host-pointer C-ABI call
+(ft_proposed_batch_host) with pinned host buffers over the full shard: every
+step copies x in and sin/cos/tan out.  `e2e_variants` adds the reference-shaped
+seams: the three single-output calls ft_proposed_{sin,cos,tan}_batch on
+pageable (malloc'd) buffers -- what fasttrig::gpu::proposed_*_batch with
+std::vector does -- and the fused call on pageable buffers.  `cpu_baseline`
+(rank 0, N=1) and `--impl reference` time the reference's own CPU
+implementation (oracle/_ref: the unmodified reference headers, all host
+threads) on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -217,23 +230,71 @@ def host_cpu_model() -> str:
     return "unknown"
 
 
+# ------------------------------------------------------------------ shared
+# Timed steps per extra config (~0.2-1 s of timed work each at N=1).
+CONFIG_STEPS = {"cfg1": 2000, "cfg2": 600, "cfg3": 1000, "cfg4_f32": 400, "cfg4_f64": 300, "cfg5": 20}
+EXTRA_CONFIGS = ("cfg1", "cfg3", "cfg4_f32", "cfg4_f64", "cfg5")
+L2_BYTES = 126 * 1000 * 1000
+
+
+def plan(w, world: int, rank: int, elements: int = 0):
+    """(n on this rank, global offset, scaling, total elements) for workload w.
+    cfg5 is one fixed global array split over the ranks (strong); the others give
+    every rank its own shard of w.n (or `elements`) elements (weak)."""
+    from paper_2502_10831_b200.configs import shard
+
+    if w.name == "cfg5":
+        total = elements or w.n
+        lo, hi = shard(total, rank, world)
+        return hi - lo, lo, "strong", total
+    n = elements or w.n
+    return n, rank * n, "weak", n * world
+
+
+def config_dict(w, n: int, world: int, policy: str, flush: bool) -> dict:
+    """The `config` object of a line: identical for our arm and the reference arm."""
+    names = [nm for j, nm in enumerate(("sin", "cos", "tan")) if w.mask & (1 << j)]
+    d = {"workload": w.name, "description": w.note, "elements_per_gpu": n, "outputs": names,
+         "sqrt_mode": "fisr(1) (SqrtMode{} default)" if w.kind == 0 else f"Taylor-{w.n_terms}",
+         "parallelism": f"dp{world} contiguous shards, no data exchange",
+         "l2": (f"x ({w.itemsize * n / 2**20:.0f} MiB) smaller than L2: 2x-L2 flush between timed steps"
+                if flush else f"inputs larger than L2 (x + outputs = {w.bytes_per_elem * n / 2**30:.1f} GiB "
+                              "per GPU vs 126 MB L2); no flush")}
+    if w.itemsize == 4:
+        d["f32_policy"] = policy
+    return d
+
+
+def needs_flush(w, n: int) -> bool:
+    return w.itemsize * n < L2_BYTES
+
+
 # ------------------------------------------------------------------ reference arm
+def reference_sample(steps: int, warmup: int) -> int:
+    """Elements per reference step: the whole 2^28 headline shard when the run is
+    short, else a power-of-two slice so that (steps + warmup) steps stay within
+    a few minutes; deterministic (does not depend on the host's speed)."""
+    n = 1 << 28
+    total = max(1, steps + warmup)
+    while n > (1 << 20) and n * total > (1 << 28) * 64:
+        n >>= 1
+    return n
+
+
 def run_reference(args) -> None:
     rank = env_int("RANK", 0)
     if rank != 0:
         return  # the reference arm is single-process CPU work; other ranks idle
-    import numpy as np
-
     from oracle import oracle as O
     from paper_2502_10831_b200.configs import CONFIGS
 
     w = CONFIGS[args.config]
     threads = O.ncpu()
-    total_steps = args.steps + args.warmup
-    per_step = max(0.2, min(2.0, 120.0 / max(total_steps, 1)))
-    # sample inputs: the first elements of the same seeded stream
-    rate, kind, n, _, x = cpu_rate(host_inputs(w), w.mask, threads, per_step)
+    n_cfg, _, scaling, _ = plan(w, 1, 0, args.elements)
+    n = min(n_cfg, reference_sample(args.steps, args.warmup))
+    kind = "reference" if O.ref_available() else "port"
     impl = "ref" if kind == "reference" else "port"
+    x = host_inputs(w)(n)
     for _ in range(args.warmup):
         O.proposed(x, w.mask, threads=threads, impl=impl)
     times = []
@@ -243,16 +304,16 @@ def run_reference(args) -> None:
         times.append(time.perf_counter() - t0)
     ms = 1e3 * statistics.mean(times)
     value = n / (ms / 1e3) / 1e9
-    sample = (f"first {n} elements of {w.name} ({w.note}); fused sin+cos+tan via the scalar "
+    sample = (f"first {n} elements of {w.name} per step ({w.note}); fused sin+cos+tan via the scalar "
               f"reference calls, contiguous partition over {threads} threads; {host_cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Gelem/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64" if w.itemsize == 8 else "f32", "data": "synthetic",
-        "config": {"workload": w.name, "description": w.note, "elements_per_step": n},
+        "config": config_dict(w, n_cfg, args.gpus, args.f32_policy, needs_flush(w, n_cfg)),
         "cpu_baseline": {"value": round(value, 6), "unit": "Gelem/s", "cores": threads,
-                         "kind": kind, "sample": sample,
+                         "kind": kind, "sample": sample, "elements_per_step": n,
                          "api_batch_single_thread_gelem_s": api_single_thread_rate(w)},
         "e2e": {"value": round(value, 6), "unit": "Gelem/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -262,43 +323,93 @@ def run_reference(args) -> None:
 
 
 # ------------------------------------------------------------------ our arm
-def run_ours(args) -> None:
-    import numpy as np
+class Ctx:
+    """Per-process state of our arm: rank layout, device, collectives."""
+
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+
+        self.args = args
+        self.world = env_int("WORLD_SIZE", 1)
+        self.rank = env_int("RANK", 0)
+        local = env_int("LOCAL_RANK", 0)
+        if self.world != args.gpus and self.world > 1:
+            print(f"warning: WORLD_SIZE={self.world} but --gpus {args.gpus}", file=sys.stderr)
+        ndev = torch.cuda.device_count()
+        self.device_index = local % max(1, ndev)  # gloo test runs put several ranks on one GPU
+        torch.cuda.set_device(self.device_index)
+        self.dev = torch.device("cuda", self.device_index)
+        launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # torchrun
+        self.backend = args.backend
+        if self.world > 1 or launched:
+            if self.backend == "nccl":
+                # communicator INIT lines (rank count, NVLS / ring setup) into the log
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group("gloo")
+        self.dist = dist
+
+    @property
+    def coll_device(self):
+        return self.dev if self.backend == "nccl" else "cpu"
+
+    def barrier(self):
+        if self.dist.is_initialized():
+            self.dist.barrier()
+
+    def max_over_ranks(self, v: float) -> float:
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64, device=self.coll_device)
+        if self.dist.is_initialized() and self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def time_steps(step, k: int, stream, flush: bool) -> float:
+    """Mean device time of one step (ms) over k steps, CUDA events on `stream`.
+    flush: a 2x-L2 write before every step, outside the timed event pairs."""
     import torch
-    import torch.distributed as dist
 
     import paper_2502_10831_b200 as ft
-    from paper_2502_10831_b200 import _lib
-    from paper_2502_10831_b200.configs import CONFIGS, shard
+
+    if not flush:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / k
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+    for a, b in evs:
+        ft.l2_flush()
+        a.record(stream)
+        step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs) / k
+
+
+def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0, keep: bool = False):
+    """Generate w's shard in place, time `steps` launches of its kernel, check
+    the outputs with K3, all-reduce the statistics.  Returns (entry, state)."""
+    import torch
+
+    import paper_2502_10831_b200 as ft
     from paper_2502_10831_b200.dist import reduce_stats
 
-    world = env_int("WORLD_SIZE", 1)
-    rank = env_int("RANK", 0)
-    local = env_int("LOCAL_RANK", 0)
-    if world != args.gpus and world > 1:
-        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ  # torchrun
-    if world > 1 or launched:
-        dist.init_process_group("nccl", device_id=dev)
-    _lib.lib()  # fail loudly if the CUDA library is missing
-
-    w = CONFIGS[args.config]
+    n, lo, scaling, total = plan(w, ctx.world, ctx.rank, elements)
     tdt = torch.float32 if w.itemsize == 4 else torch.float64
-    n = args.elements or w.n
-    if args.config == "cfg5":
-        lo, hi = shard(w.n, rank, world)  # strong: one fixed 2^33 array
-        n = hi - lo
-        scaling = "strong"
-    else:
-        lo, hi = rank * n, (rank + 1) * n  # weak: a fixed shard per GPU
-        scaling = "weak"
     stream = torch.cuda.current_stream()
     x = ft.gen_inputs(n, tdt, w.dist, w.lo, w.hi, w.seed, lo)
     names = [nm for j, nm in enumerate(("sin", "cos", "tan")) if w.mask & (1 << j)]
     out = {nm: torch.empty_like(x) for nm in names}
     mode = ft.SqrtMode()
+    flush = needs_flush(w, n)
 
     def step():
         if w.kind == 0:
@@ -306,100 +417,166 @@ def run_ours(args) -> None:
         else:
             ft.taylor_eval(x, w.n_terms, w.mask, out=out)
 
-    def barrier():
-        if dist.is_initialized():
-            dist.barrier()
+    with ft.f32_policy(policy):
+        clocks = ClockSampler(ctx.device_index)  # samples from warm-up start to timed-region end
+        clocks.start()
+        clocks.mark()
+        for _ in range(max(warmup, 3)):
+            step()
+        torch.cuda.synchronize()
+        ctx.barrier()
+        torch.cuda.synchronize()
+        l0 = ft.launch_count()
+        ms_local = time_steps(step, steps, stream, flush)
+        ctx.barrier()
+        launches = ft.launch_count() - l0 - (steps if flush else 0)
+        clk = clocks.stop()
+    ms = ctx.max_over_ranks(ms_local)
+    value = total / (ms / 1e3) / 1e9
 
-    clocks = ClockSampler(local)  # samples from warm-up start to timed-region end (GPU loaded)
-    clocks.start()
-    clocks.mark()
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    l0 = ft.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    launches = ft.launch_count() - l0
-    clk = clocks.stop()
-    ms_local = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    elems_total = n * world if scaling == "weak" else w.n
-    value = elems_total / (ms / 1e3) / 1e9
-
-    # ---- roofline of the dominant (only) kernel in the step
     peak, peak_src = peaks()
-    bytes_per_launch = w.bytes_per_elem * n
-    achieved = bytes_per_launch / (ms_local / 1e3) / 1e9
+    achieved = w.bytes_per_elem * n / (ms_local / 1e3) / 1e9
+    traffic = ncu_traffic(w.name)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed "
+                                   "ncu --set full capture (profiles/ncu_k1_summary.json; static, not measured "
+                                   "in this run)") if traffic else None,
+                "peak_source": peak_src, "algorithmic_bytes_per_elem": w.bytes_per_elem,
+                "kernel": ("k_proposed (K1)" if w.kind == 0 else "k_taylor (K2)")
+                + (" relaxed f32" if w.itemsize == 4 and policy == "ulp2" else "")}
 
-    # ---- accuracy: K3 over the whole shard, NCCL-reduced (max / sum)
     st = ft.parity_reduce(x, out, w.mask, kind=w.kind, mode=mode, n_terms=w.n_terms, ulp_tol=2)
-    st = reduce_stats(st, device=dev)  # the path's only collective: 64 B of stats
+    st = reduce_stats(st, device=ctx.coll_device)  # the path's only collective: 312 B of stats
     accuracy = {
-        "checked": int(st["n_checked"]), "max_ulp_vs_oracle": st["max_ulp"],
-        "over_2ulp": st["n_over_tol"],
+        "checked": int(st["n_checked"]), "max_ulp_vs_oracle": st["max_ulp"], "tolerance_ulp": 2,
+        "over_2ulp": st["n_over_tol"], "bit_mismatch_vs_oracle": st["n_bit_mismatch"],
         "max_abs_err_vs_libm": st["max_abs_vs_libm"], "max_rel_err_vs_libm": st["max_rel_vs_libm"],
         "avg_abs_err_vs_libm": [s_ / max(1, c) for s_, c in zip(st["sum_abs_vs_libm"], st["n_finite_libm"])],
         "max_abs_err_vs_oracle": st["max_abs_vs_oracle"], "inf_count": st["n_inf"],
         "nan_count": st["n_nan"], "checksum": st["checksum"], "outputs": names,
         "oracle": "device restatement of the reference (ft_mirror_*), bitwise-pinned to the CPU oracle",
     }
+    entry = {"value": round(value, 4), "unit": "Gelem/s", "per_gpu_gelem_s": round(n / (ms / 1e3) / 1e9, 4),
+             "ms_per_step": round(ms, 5), "steps": steps, "warmup": max(warmup, 3), "scaling": scaling,
+             "dtype": "f64" if w.itemsize == 8 else "f32",
+             "config": config_dict(w, n, ctx.world, policy, flush), "roofline": roofline,
+             "fp64_roof": fp64_roof(w.name, n / (ms_local / 1e3) / 1e9), "gpu_launches": int(launches),
+             "clocks": clk, "accuracy": accuracy}
+    state = {"x": x, "out": out, "n": n, "names": names, "tdt": tdt} if keep else None
+    if not keep:
+        del x, out
+        torch.cuda.empty_cache()
+    return entry, state
 
-    # ---- e2e through the public host-pointer C-ABI call (pinned host buffers)
-    e2e = None
-    if not args.no_e2e:
-        n_e2e = min(n, args.e2e_elements)
-        xh = torch.empty(n_e2e, dtype=tdt, pin_memory=True)
-        xh.copy_(x[:n_e2e])
-        outs_h = {nm: torch.empty(n_e2e, dtype=tdt, pin_memory=True) for nm in names}
-        ptr = [outs_h[nm].data_ptr() if nm in outs_h else None for nm in ("sin", "cos", "tan")]
-        L = _lib.lib()
-        dtc = _lib.FT_F32 if w.itemsize == 4 else _lib.FT_F64
 
-        def e2e_step():
-            if w.kind == 0:
-                _lib.check(L.ft_proposed_batch_host(dtc, xh.data_ptr(), n_e2e, w.mask, mode.c(), *ptr))
-            else:
-                _lib.check(L.ft_taylor_batch_host(dtc, xh.data_ptr(), n_e2e, w.mask, w.n_terms, *ptr))
+def e2e_pinned(ctx: Ctx, w, state, steps: int, n_e2e: int) -> dict:
+    """The headline metric through the fused host-pointer C-ABI call, pinned
+    host buffers, H2D of x and D2H of every output inside each timed step."""
+    import torch
 
-        e2e_step()  # warm (allocates the pipeline buffers)
-        barrier()
+    from paper_2502_10831_b200 import _lib
+
+    names, tdt = state["names"], state["tdt"]
+    xh = torch.empty(n_e2e, dtype=tdt, pin_memory=True)
+    xh.copy_(state["x"][:n_e2e])
+    outs_h = {nm: torch.empty(n_e2e, dtype=tdt, pin_memory=True) for nm in names}
+    ptr = [outs_h[nm].data_ptr() if nm in outs_h else None for nm in ("sin", "cos", "tan")]
+    L = _lib.lib()
+    dtc = _lib.FT_F32 if w.itemsize == 4 else _lib.FT_F64
+    mode = _lib.SqrtModeC(1, 1)
+
+    def call():
+        if w.kind == 0:
+            _lib.check(L.ft_proposed_batch_host(dtc, xh.data_ptr(), n_e2e, w.mask, mode, *ptr))
+        else:
+            _lib.check(L.ft_taylor_batch_host(dtc, xh.data_ptr(), n_e2e, w.mask, w.n_terms, *ptr))
+
+    call()  # warm (allocates the pipeline buffers)
+    ctx.barrier()
+    times = []
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        call()  # blocking: returns with results in host memory
+        times.append(time.perf_counter() - t0)
+    t = ctx.max_over_ranks(statistics.mean(times))
+    del xh, outs_h
+    return {"value": round(n_e2e * ctx.world / t / 1e9, 6), "unit": "Gelem/s",
+            "h2d_bytes_per_step": n_e2e * w.itemsize, "d2h_bytes_per_step": n_e2e * w.itemsize * len(names),
+            "elements_per_step_per_gpu": n_e2e, "steps": steps,
+            "timing": "host wall clock around the blocking fused C-ABI call (pinned buffers), max over ranks"}
+
+
+def e2e_pageable(ctx: Ctx, w, state, steps: int, n_e2e: int) -> dict:
+    """The reference-shaped seams on pageable host memory (numpy = malloc'd, as a
+    std::vector is): (a) the three single-output calls ft_proposed_{sin,cos,tan}_batch
+    per step -- what fasttrig::gpu::proposed_*_batch does --, (b) the fused call."""
+    import numpy as np
+    import torch
+
+    from paper_2502_10831_b200 import _lib
+
+    L = _lib.lib()
+    mode = _lib.SqrtModeC(1, 1)
+    res = {}
+    if w.kind != 0 or w.itemsize != 8 or w.mask != 7:
+        return res
+    x = state["x"][:n_e2e].cpu().numpy()
+    outs = {nm: np.empty_like(x) for nm in ("sin", "cos", "tan")}
+    fns = (L.ft_proposed_sin_batch, L.ft_proposed_cos_batch, L.ft_proposed_tan_batch)
+
+    def three():
+        for f, nm in zip(fns, ("sin", "cos", "tan")):
+            _lib.check(f(x.ctypes.data, n_e2e, mode, outs[nm].ctypes.data))
+
+    def fused():
+        _lib.check(L.ft_proposed_batch_host(_lib.FT_F64, x.ctypes.data, n_e2e, 7, mode,
+                                            *[outs[nm].ctypes.data for nm in ("sin", "cos", "tan")]))
+
+    for name, fn, h2d in (("api_single_output_x3_pageable", three, 3), ("fused_pageable", fused, 1)):
+        fn()  # warm
+        ctx.barrier()
         times = []
-        for _ in range(args.e2e_steps):
+        for _ in range(steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            e2e_step()  # blocking: returns with results in host memory
+            fn()
             times.append(time.perf_counter() - t0)
-        te = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_tot = n_e2e * world if scaling == "weak" else n_e2e * world
-        e2e = {"value": round(e2e_tot / float(te.item()) / 1e9, 6), "unit": "Gelem/s",
-               "h2d_bytes_per_step": n_e2e * w.itemsize,
-               "d2h_bytes_per_step": n_e2e * w.itemsize * len(names),
-               "elements_per_step_per_gpu": n_e2e, "steps": args.e2e_steps,
-               "timing": "host wall clock around the blocking C-ABI call (pinned buffers)"}
-        del xh, outs_h
+        t = ctx.max_over_ranks(statistics.mean(times))
+        res[name] = {"value": round(n_e2e * ctx.world / t / 1e9, 6), "unit": "Gelem/s",
+                     "h2d_bytes_per_step": h2d * n_e2e * 8, "d2h_bytes_per_step": 3 * n_e2e * 8,
+                     "elements_per_step_per_gpu": n_e2e, "steps": steps}
+    return res
+
+
+def run_ours(args) -> None:
+    import torch
+
+    from paper_2502_10831_b200 import _lib
+    from paper_2502_10831_b200.configs import CONFIGS
+
+    ctx = Ctx(args)
+    _lib.lib()  # fail loudly if the CUDA library is missing
+    w = CONFIGS[args.config]
+    head, state = measure(ctx, w, args.steps, args.warmup, args.f32_policy, args.elements, keep=True)
+
+    e2e, e2e_var = None, None
+    if not args.no_e2e:
+        n_e2e = min(state["n"], args.e2e_elements or state["n"])
+        e2e = e2e_pinned(ctx, w, state, args.e2e_steps, n_e2e)
+        e2e_var = e2e_pageable(ctx, w, state, args.e2e_steps, n_e2e) or None
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu:
         from oracle import oracle as O
 
         threads = O.ncpu()
         if w.dist == 0:
             get = host_inputs(w)
         else:
-            xh_all = x.cpu().numpy()
+            xh_all = state["x"].cpu().numpy()
             get = lambda m: xh_all[:m]  # noqa: E731 -- device-generated stress inputs
         rate, kind, ns, sec, _ = cpu_rate(get, w.mask, threads, 10.0)
         cpu = {"value": round(rate, 6), "unit": "Gelem/s", "cores": threads, "kind": kind,
@@ -407,35 +584,34 @@ def run_ours(args) -> None:
                          f"sin+cos+tan via the scalar reference calls over {threads} threads; "
                          f"{host_cpu_model()}",
                "api_batch_single_thread_gelem_s": api_single_thread_rate(w)}
+    del state
+    torch.cuda.empty_cache()
 
-    if rank == 0:
+    # ---- every other BASELINE config in the same run
+    extra = {}
+    sel = args.configs
+    names = ([] if sel == "none" else [c for c in EXTRA_CONFIGS if c != w.name] if sel == "auto" and w.name == "cfg2"
+             else [] if sel == "auto" else [c for c in sel.split(",") if c and c != w.name])
+    for c in names:
+        k = args.config_steps or CONFIG_STEPS.get(c, 100)
+        e, _ = measure(ctx, CONFIGS[c], k, min(args.warmup, 10), args.f32_policy)
+        extra[c] = e
+
+    if ctx.rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 4), "unit": "Gelem/s", "n_gpus": world,
-            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms, 5),
-            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
-            "dtype": "f64" if w.itemsize == 8 else "f32", "data": "synthetic",
-            "config": {"workload": w.name, "description": w.note, "elements_per_gpu": n,
-                       "outputs": names, "sqrt_mode": "fisr(1) (SqrtMode{} default)",
-                       "parallelism": f"dp{world} contiguous shards, no data exchange",
-                       "l2": "inputs larger than L2 (x + outputs = "
-                             f"{w.bytes_per_elem * n / 2**30:.1f} GiB per GPU vs 126 MB L2); no flush"},
-            "per_gpu_gelem_s": round(n / (ms / 1e3) / 1e9, 4),
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": ncu_traffic(w.name), "peak_source": peak_src,
-                         "algorithmic_bytes_per_elem": w.bytes_per_elem,
-                         "kernel": "k_proposed (K1)" if w.kind == 0 else "k_taylor (K2)"},
-            "fp64_roof": fp64_roof(w.name, n / (ms / 1e3) / 1e9),
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "clocks": clk,
-            "accuracy": accuracy,
+            "metric": METRIC, "value": head["value"], "unit": "Gelem/s", "n_gpus": ctx.world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": head["scaling"], "vs_baseline": None,
+            "dtype": head["dtype"], "data": "synthetic", "config": head["config"],
+            "per_gpu_gelem_s": head["per_gpu_gelem_s"], "roofline": head["roofline"],
+            "fp64_roof": head["fp64_roof"], "cpu_baseline": cpu, "e2e": e2e, "e2e_variants": e2e_var,
+            "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "accuracy": head["accuracy"],
+            "configs": extra or None,
         }
         print(json.dumps(line), flush=True)
-    if dist.is_initialized():
-        dist.barrier()
-        dist.destroy_process_group()
+    if ctx.dist.is_initialized():
+        ctx.dist.barrier()
+        ctx.dist.destroy_process_group()
 
 
 def main() -> None:
@@ -445,10 +621,19 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--elements", type=int, default=0, help="override elements per GPU")
+    ap.add_argument("--configs", default="auto",
+                    help="extra configs timed in the same run: auto (all others when --config cfg2), "
+                         "none, or a comma list")
+    ap.add_argument("--config-steps", type=int, default=0,
+                    help="timed steps of every extra config (default: CONFIG_STEPS)")
+    ap.add_argument("--elements", type=int, default=0,
+                    help="override elements per GPU (weak configs) / of the global array (cfg5)")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process-group backend; gloo only for tests that run several ranks on one GPU")
+    ap.add_argument("--f32-policy", choices=["ulp2", "bitwise"], default="ulp2")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-elements", type=int, default=1 << 26,
-                    help="elements per rank per e2e step (pinned host buffers of this size)")
+    ap.add_argument("--e2e-elements", type=int, default=0,
+                    help="elements per rank per e2e step (default: the whole shard)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -10,6 +10,9 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <memory>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -225,13 +228,113 @@ int stage_reserve(Staging& g, std::size_t bytes) {
   return FT_OK;
 }
 
-// A batch of memcpys split into ~4 MiB parts over up to 16 host threads (one
-// core moves ~10 GB/s; the staged path needs ~32 B per element through memory).
+// A batch of memcpys split into ~4 MiB parts over a persistent pool of up to 16
+// host threads (one core moves ~10 GB/s; the staged path needs ~32 B per
+// element through memory).  The pool replaces per-chunk std::thread spawning
+// (~2000 thread creations per 2^28-element call); the calling thread works on
+// its own job too, and concurrent callers (one per device in host_sharded)
+// share the workers.
 struct Copy {
   void* dst;
   const void* src;
   std::size_t bytes;
 };
+
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+
+  void run(std::vector<Copy> parts) {
+    if (parts.empty()) return;
+    auto job = std::make_shared<Job>();
+    job->parts = std::move(parts);
+    if (!th_.empty() && job->parts.size() > 1) {
+      std::lock_guard<std::mutex> lk(mu_);
+      q_.push_back(job);
+      cv_.notify_all();
+    }
+    work(*job);
+    std::unique_lock<std::mutex> lk(job->m);
+    job->cv.wait(lk, [&] { return job->done.load() == job->parts.size(); });
+    lk.unlock();
+    std::lock_guard<std::mutex> ql(mu_);
+    for (auto it = q_.begin(); it != q_.end(); ++it)
+      if (*it == job) {
+        q_.erase(it);
+        break;
+      }
+  }
+
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      cv_.notify_all();
+    }
+    for (auto& t : th_) t.join();
+  }
+
+ private:
+  struct Job {
+    std::vector<Copy> parts;
+    std::atomic<std::size_t> next{0}, done{0};
+    std::mutex m;
+    std::condition_variable cv;
+  };
+
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned n = std::min(16u, hw ? hw : 1u);
+    for (unsigned i = 1; i < n; ++i) th_.emplace_back([this] { worker(); });
+  }
+
+  static void work(Job& j) {
+    std::size_t i;
+    while ((i = j.next.fetch_add(1)) < j.parts.size()) {
+      std::memcpy(j.parts[i].dst, j.parts[i].src, j.parts[i].bytes);
+      if (j.done.fetch_add(1) + 1 == j.parts.size()) {
+        std::lock_guard<std::mutex> lk(j.m);
+        j.cv.notify_all();
+      }
+    }
+  }
+
+  void worker() {
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+      if (stop_) return;
+      std::shared_ptr<Job> j;
+      for (auto& cand : q_)
+        if (cand->next.load() < cand->parts.size()) {
+          j = cand;
+          break;
+        }
+      if (!j) {  // every queued job is fully claimed: wait for the next one
+        cv_.wait(lk, [&] {
+          if (stop_) return true;
+          for (auto& cand : q_)
+            if (cand->next.load() < cand->parts.size()) return true;
+          return false;
+        });
+        continue;
+      }
+      lk.unlock();
+      work(*j);
+      lk.lock();
+    }
+  }
+
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::shared_ptr<Job>> q_;
+  std::vector<std::thread> th_;
+  bool stop_ = false;
+};
+
 void parallel_copies(const std::vector<Copy>& copies) {
   const std::size_t part = std::size_t(4) << 20;
   std::vector<Copy> parts;
@@ -239,16 +342,7 @@ void parallel_copies(const std::vector<Copy>& copies) {
     for (std::size_t lo = 0; lo < c.bytes; lo += part)
       parts.push_back({static_cast<char*>(c.dst) + lo, static_cast<const char*>(c.src) + lo,
                        std::min(part, c.bytes - lo)});
-  if (parts.empty()) return;
-  unsigned hw = std::thread::hardware_concurrency();
-  const std::size_t nt = std::min<std::size_t>({16, hw ? hw : 1, parts.size()});
-  auto work = [&](std::size_t t) {
-    for (std::size_t i = t; i < parts.size(); i += nt) std::memcpy(parts[i].dst, parts[i].src, parts[i].bytes);
-  };
-  std::vector<std::thread> th;
-  for (std::size_t t = 1; t < nt; ++t) th.emplace_back(work, t);
-  work(0);
-  for (auto& t : th) t.join();
+  CopyPool::get().run(std::move(parts));
 }
 
 template <class Launch>

@@ -368,8 +368,12 @@ __global__ void __launch_bounds__(kThreads, (kMinBlocksK2<T, MASK>)) k_taylor(co
 #ifndef FT_MINB_RELAX_TAYLOR
 #define FT_MINB_RELAX_TAYLOR 5
 #endif
+#ifndef FT_MINB_RELAX_TAN
+#define FT_MINB_RELAX_TAN 4  // tan-only relaxed kernels (52 registers at 4)
+#endif
 template <int SQ, unsigned MASK, bool SEG>
-__global__ void __launch_bounds__(kThreads, FT_MINB_RELAX) k_proposed_relaxed(const EvalArgs a) {
+__global__ void __launch_bounds__(kThreads, MASK == kTan ? FT_MINB_RELAX_TAN : FT_MINB_RELAX)
+    k_proposed_relaxed(const EvalArgs a) {
   __shared__ SmemTable tb[2];
   stage_table_relaxed<MASK, SEG>(&tb[0]);
   stage_table(&tb[1]);

@@ -32,11 +32,26 @@ def test_reference_arm_line():
                         "d2h_bytes_per_step": 0}
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["workload"] == "cfg2"
+    # key-identical to our arm's config (same function builds both)
+    assert set(d["config"]) == {"workload", "description", "elements_per_gpu", "outputs", "sqrt_mode",
+                                "parallelism", "l2"}
+    assert d["config"]["elements_per_gpu"] == 1 << 28
+    assert d["cpu_baseline"]["elements_per_step"] == 1 << 28  # 3 steps: the whole shard
+
+
+def test_reference_sample_is_deterministic():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert bench.reference_sample(2, 1) == 1 << 28
+    assert bench.reference_sample(600, 20) == 1 << 24
+    assert bench.reference_sample(10**6, 0) == 1 << 20
 
 
 @pytest.mark.gpu
 def test_our_arm_line():
-    d = run_bench("--steps", "20", "--warmup", "3", "--e2e-elements", str(1 << 22), "--e2e-steps", "2")
+    d = run_bench("--steps", "20", "--warmup", "3", "--e2e-elements", str(1 << 22), "--e2e-steps", "2",
+                  "--configs", "cfg1,cfg3,cfg4_f32")
     assert BASE_KEYS <= set(d) and "roofline" in d and "clocks" in d
     assert d["n_gpus"] == 1 and d["scaling"] == "weak" and d["dtype"] == "f64"
     assert d["gpu_launches"] == 20
@@ -46,4 +61,16 @@ def test_our_arm_line():
     assert d["e2e"]["h2d_bytes_per_step"] == (1 << 22) * 8
     assert d["e2e"]["d2h_bytes_per_step"] == 3 * (1 << 22) * 8
     assert d["accuracy"]["max_ulp_vs_oracle"] == [0, 0, 0]
+    assert d["accuracy"]["bit_mismatch_vs_oracle"] == [0, 0, 0]
     assert d["cpu_baseline"]["value"] > 0
+    ev = d["e2e_variants"]
+    assert set(ev) == {"api_single_output_x3_pageable", "fused_pageable"}
+    assert all(v["value"] > 0 for v in ev.values())
+    assert set(d["configs"]) == {"cfg1", "cfg3", "cfg4_f32"}
+    for name, c in d["configs"].items():
+        assert c["value"] > 0 and c["dtype"] == "f32" and c["config"]["workload"] == name
+        assert 0 < c["roofline"]["frac"] < 1.2
+        assert c["accuracy"]["over_2ulp"] == [0, 0, 0] and max(c["accuracy"]["max_ulp_vs_oracle"]) <= 2
+        assert c["config"]["f32_policy"] == "ulp2"
+    assert "flush" in d["configs"]["cfg1"]["config"]["l2"]
+    assert d["configs"]["cfg1"]["gpu_launches"] == 2000

@@ -116,3 +116,60 @@ def test_reduce_stats_single_process_is_identity():
     red = reduce_stats(st)
     for k in st:
         assert red[k] == st[k] or np.allclose(red[k], st[k]), k
+
+
+def test_reduce_stats_clamps_nan_ulp_and_sums_bit_mismatches():
+    """max_ulp of a NaN-vs-number pair (K3 reports 2^64-1) stays huge after the
+    int64 reduction; n_bit_mismatch is summed like the other counters."""
+    st = shard_stats(0, 1)
+    st["max_ulp"] = [(1 << 64) - 1, 3, 0]
+    st["n_bit_mismatch"] = [5, 0, 1]
+    red = reduce_stats(st)
+    assert red["max_ulp"] == [(1 << 63) - 1, 3, 0]
+    assert red["n_bit_mismatch"] == [5, 0, 1]
+
+
+def _bench_json(cmd: list[str], timeout: int = 900) -> dict:
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT,
+                       env={**os.environ, "PYTHONPATH": ROOT})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_real_k3_stats_equal_one_rank():
+    """bench.py under torchrun with 2 ranks (gloo, both on the one GPU of the
+    lease): every rank runs K1 + K3 on its contiguous shard of one cfg5-recipe
+    array and the ranks all-reduce the real K3 statistics; the reduced checksums,
+    counts and maxima equal a single rank's pass over the whole array, and the
+    full 2^33-element array reproduces round 1's bit-exact checksums."""
+    import sys
+
+    from conftest import ROOT
+
+    common = ["--config", "cfg5", "--elements", str(1 << 30), "--configs", "none", "--no-e2e", "--no-cpu",
+              "--steps", "3", "--warmup", "3", "--f32-policy", "bitwise"]
+    two = _bench_json([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                       "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+                       os.path.join(ROOT, "bench.py"), "--gpus", "2", "--backend", "gloo", *common])
+    one = _bench_json([sys.executable, os.path.join(ROOT, "bench.py"), *common])
+    assert two["n_gpus"] == 2 and two["scaling"] == "strong"
+    assert two["config"]["elements_per_gpu"] == 1 << 29 and one["config"]["elements_per_gpu"] == 1 << 30
+    a2, a1 = two["accuracy"], one["accuracy"]
+    for k in ("checked", "checksum", "inf_count", "nan_count", "max_ulp_vs_oracle", "max_abs_err_vs_libm",
+              "max_rel_err_vs_libm", "bit_mismatch_vs_oracle"):
+        assert a2[k] == a1[k], k
+    assert a1["checked"] == 1 << 30 and a1["max_ulp_vs_oracle"] == [0, 0, 0]
+    full = _bench_json([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "cfg5", "--configs", "none",
+                        "--no-e2e", "--no-cpu", "--steps", "2", "--warmup", "3", "--f32-policy", "bitwise"])
+    assert full["accuracy"]["checked"] == 1 << 33
+    # profiles/r01e_cfg5_full.json (round 1, bit-exact kernel)
+    assert full["accuracy"]["checksum"] == [18298921530744543647, 18299087910619986952, 18375888137372184031]
