@@ -1,6 +1,6 @@
 """Summarise one evidence tag's ncu --set full captures into profiles/.
 
-    python tools/ncu_summarize.py r01g [--update-json]
+    python tools/ncu_summarize.py r01g [--update-json] [--out DIR] [--from-csv DIR]
 
 For each gpurun_out/<tag>_<kernel>_<cfgN>.ncu-rep (e.g. r02d_k1r_cfg1) writes
 profiles/<tag>_<name>_ncu_summary.txt (the metrics quoted in DESIGN.md /
@@ -22,15 +22,21 @@ WORKLOADS = {"cfg1": ("cfg1", 1 << 24), "cfg2": ("cfg2", 1 << 28), "cfg3": ("cfg
              "cfg4f32": ("cfg4_f32", 1 << 28), "cfg4f64": ("cfg4_f64", 1 << 28), "cfg5": ("cfg5", 1 << 30)}
 
 
-def captures(tag):
-    """{name: (workload, n)} for every gpurun_out/<tag>_<name>.ncu-rep."""
+def captures(tag, csv_dir=None):
+    """{name: (workload, n, source)} for every gpurun_out/<tag>_<name>.ncu-rep, or
+    every <csv_dir>/<tag>_<name>_ncu_raw.csv (summaries written on the GPU box)."""
     import glob
     out = {}
-    for f in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", f"{tag}_*.ncu-rep"))):
-        name = os.path.basename(f)[len(tag) + 1:-len(".ncu-rep")]
+    if csv_dir:
+        files = sorted(glob.glob(os.path.join(csv_dir, f"{tag}_*_ncu_raw.csv")))
+        names = [os.path.basename(f)[len(tag) + 1:-len("_ncu_raw.csv")] for f in files]
+    else:
+        files = sorted(glob.glob(os.path.join(ROOT, "gpurun_out", f"{tag}_*.ncu-rep")))
+        names = [os.path.basename(f)[len(tag) + 1:-len(".ncu-rep")] for f in files]
+    for f, name in zip(files, names):
         wl = WORKLOADS.get(name.rsplit("_", 1)[-1])
         if wl:
-            out[name] = wl
+            out[name] = (*wl, f)
     return out
 METRICS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -56,7 +62,9 @@ def ncu_csv(rep, page):
 
 
 def raw_metrics(rep):
-    rows = list(csv.reader(io.StringIO(ncu_csv(rep, "raw"))))
+    """Raw-page metrics of a .ncu-rep, or of a saved <...>_ncu_raw.csv."""
+    text = open(rep).read() if rep.endswith(".csv") else ncu_csv(rep, "raw")
+    rows = list(csv.reader(io.StringIO(text)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
 
@@ -71,13 +79,14 @@ def to_float(s):
 def main():
     tag = sys.argv[1]
     update = "--update-json" in sys.argv
+    outdir = os.path.join(ROOT, "profiles")
+    if "--out" in sys.argv:
+        outdir = sys.argv[sys.argv.index("--out") + 1]
+        os.makedirs(outdir, exist_ok=True)
     js_path = os.path.join(ROOT, "profiles", "ncu_k1_summary.json")
     js = json.load(open(js_path)) if os.path.exists(js_path) else {}
-    for name, (wl, n) in captures(tag).items():
-        rep = os.path.join(ROOT, "gpurun_out", f"{tag}_{name}.ncu-rep")
-        if not os.path.exists(rep):
-            print("missing", rep)
-            continue
+    csv_dir = sys.argv[sys.argv.index("--from-csv") + 1] if "--from-csv" in sys.argv else None
+    for name, (wl, n, rep) in captures(tag, csv_dir).items():
         m = raw_metrics(rep)
         lines = []
         for k in METRICS:
@@ -89,15 +98,23 @@ def main():
                          and to_float(v[0]) is not None), key=lambda t: -t[1])
         for k, v in stalls[:12]:
             lines.append(f"  {k:<78} {v}")
-        txt = os.path.join(ROOT, "profiles", f"{tag}_{name}_ncu_summary.txt")
+        txt = os.path.join(outdir, f"{tag}_{name}_ncu_summary.txt")
         open(txt, "w").write("\n".join(lines) + "\n")
-        open(os.path.join(ROOT, "profiles", f"{tag}_{name}_ncu_details.csv"), "w").write(ncu_csv(rep, "details"))
+        if not rep.endswith(".csv"):
+            open(os.path.join(outdir, f"{tag}_{name}_ncu_details.csv"), "w").write(ncu_csv(rep, "details"))
+            open(os.path.join(outdir, f"{tag}_{name}_ncu_raw.csv"), "w").write(ncu_csv(rep, "raw"))
         # bytes: ncu prints Mbyte/Gbyte etc.; normalise
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         rd, wr = m["dram__bytes_read.sum"], m["dram__bytes_write.sum"]
         traffic = to_float(rd[0]) * scale[rd[1]] + to_float(wr[0]) * scale[wr[1]]
         inst = to_float(m["smsp__inst_executed.sum"][0])
         fp64 = to_float(m[FP64_INST][0]) if FP64_INST in m else None
+        if fp64 is None and "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active" in m:
+            # warp instructions on the FP64 pipe = utilisation x active SM cycles x
+            # 2 warp-instructions / cycle / SM (64 FP64 lanes per SM on B200)
+            pct = to_float(m["sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"][0])
+            cyc = to_float(m["sm__cycles_active.sum"][0])
+            fp64 = pct / 100.0 * cyc * 2.0
         print(f"{name}: {m['gpu__time_duration.sum'][0]} {m['gpu__time_duration.sum'][1]}, traffic {traffic / 1e9:.4f} GB, "
               f"{inst * 32 / n:.2f} instr/elem" + (f", fp64 {fp64 * 32 / n:.2f}/elem" if fp64 else ""))
         if update:
@@ -108,6 +125,9 @@ def main():
                 js.setdefault("fp64_pipe_instr_per_elem", {})[wl] = per
             js["source"] = (f"ncu --set full --clock-control none, one launch per workload "
                             f"(profiles/{tag}_*_ncu_summary.txt)")
+            js["fp64_pipe_instr_note"] = ("FP64-pipe warp instructions x 32 / elements: "
+                                          "sm__inst_executed_pipe_fp64 % x sm__cycles_active.sum x 2 "
+                                          "warp-instructions/cycle/SM, same capture")
     if update:
         json.dump(js, open(js_path, "w"), indent=1)
         print("updated", js_path)

@@ -25,3 +25,8 @@ for spec in "k1_cfg2:k_proposed:cfg2" "k1r_cfg1:k_proposed:cfg1" "k1r_cfg3:k_pro
       python tools/run_kernel.py --config $cfg --reps 3 > $out/${tag}_ncu_$name.log 2>&1
   echo "ncu $name rc=$?"
 done
+# summaries (text + details/raw CSV) next to the outputs; the .ncu-rep files are
+# too large to bring back all at once (gpurun's 64 MiB limit): keep one
+python tools/ncu_summarize.py $tag --out $out/${tag}_ncu > $out/${tag}_ncu_summary.log 2>&1
+for f in $out/${tag}_*.ncu-rep; do case $f in *k1r_cfg1*) ;; *) rm -f $f;; esac; done
+du -sh $out
