@@ -187,10 +187,12 @@ int ft_thresholds(double* out8);
  * (same layout as ft_segment_table).  unit: 0 = the K1/K2 kernels' copy, 1 =
  * K3's, 2 = K4/K5's, 3 = the C-ABI unit's.  Synchronous. */
 int ft_device_const_table(int unit, double* out49);
-/* The shared-memory segment rows a K1 block stages, copied out by a kernel
- * (8 rows x 80 bytes: a,b,c,d,X,Y,Z as doubles, the bracket's two high words
- * as int32, the exact bracket as two doubles).  kind 0 = bit-exact rows,
- * 1..7 = the relaxed f32 rows for that output mask.  Synchronous. */
+/* The shared-memory segment rows a K1 block stages, copied out by a kernel.
+ * kind 0 = bit-exact rows: 8 x 80 bytes (a,b,c,d,X,Y,Z as doubles, the
+ * bracket's two high words as int32, the exact bracket as two doubles);
+ * kind 1..7 = the relaxed f32 rows for that output mask: 8 x 48 bytes in the
+ * first 384 bytes (a,b,c,d as doubles, the two bracket high words, 8 bytes of
+ * padding).  Synchronous. */
 int ft_device_rows(int kind, void* out640);
 /* Free the host-pointer pipeline (streams, device slots, pinned staging) and
  * the L2-flush buffer of `device` (-1: every device).  They are re-created on

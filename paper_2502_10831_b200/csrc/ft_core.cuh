@@ -746,8 +746,17 @@ __device__ __forceinline__ Out3 fast_taylor(double x, int n) {
 //     The reference's red differs from |d| only by the rounding of RN(2pi*k)
 //     (resp. RN(pi*k)) -- its other subtractions are exact (Sterbenz) -- so
 //     |red_ref - |d|| <= 2^-38 for |x| < 2^16 (2^-37.9 with d's own rounding);
-//   * the evaluation contracted to FMAs (radicand 2, each numerator and the
-//     tangent denominator 1), every other operation as in the reference.
+//   * the evaluation from the four linear coefficients only: Ns = a*red + b
+//     and Nc = c*red + d (one FMA each) are the sine and cosine numerators,
+//     the radicand is Ns^2 + Nc^2 (= X red^2 + Y red + Z identically: X, Y, Z
+//     are a^2+c^2, 2(ab+cd), b^2+d^2, segments.hpp:44-50), and with red_t = red
+//     the tangent's numerator and denominator are Ns and Nc as well
+//     (kernels.hpp:33-41).  Relative to the reference's rounded X, Y, Z and
+//     Horner steps this moves the radicand by ~2^-50 relative; the FISR seed is
+//     a continuous function of it, so the output moves by the same order.
+//     Rows shrink from 80 to 48 bytes (3 shared-memory loads, 10 wavefronts
+//     per warp instead of 16 -- cfg1 was L1-throughput bound at 84%) and the
+//     tangent needs no FMAs of its own.
 //
 // Certification (else the lane takes the bit-exact path, relaxed_slow):
 //   * |x| < 2^16;
@@ -763,18 +772,31 @@ __device__ __forceinline__ Out3 fast_taylor(double x, int n) {
 //     certain when hi(red) != hi(guard) (the guard sits >= 2.3e-7 inside its
 //     high-word bucket) and hi(red) < hi(pi/2) (row 5's bracket; m's parity
 //     can flip only within ~2^-38 of pi/2).
-// Segment choice is g, the certified row.  tests/test_parity_gpu.py checks all
-// 2^32 float inputs against the bit-exact kernel (<= 1 ulp observed).
+// Segment choice is g, the certified row.  tests/test_f32_exhaustive_gpu.py
+// checks all 2^32 float inputs against the bit-exact kernels and the
+// reference library (<= 1 ulp observed, segments identical).
 constexpr float kRelaxMaxAbs = 65536.0f;  // 2^16
 constexpr int kHiRelaxLo = 0x3f400000;    // hi(2^-11)
 constexpr int kHiRelaxCos = 0x3ff91ffb;   // hi(pi/2 - 2^-11)
 constexpr int kHiGuard = 0x3ff91de2;      // hi(kFast.guard)
 constexpr double kRintMagic = 0x1.8p52;   // 1.5 * 2^52: RN(v + magic) - magic = rint(v), |v| < 2^51
 
-// The relaxed kernels' rows: coefficients as SmemTable, brackets narrowed by
-// the sensitivity bounds above for the functions MASK evaluates.
+// Relaxed rows: the linear coefficients and the high-word bracket narrowed by
+// the sensitivity bounds above for the functions MASK evaluates.  48-byte
+// stride: a warp's LDS.128 (8 lanes per phase) and LDS.64 (16 lanes) of any
+// row mix fall in disjoint banks (row k starts at word 12k: 0,12,24,4,16,28,8,20).
+struct alignas(16) RelaxRow {
+  double a, b, c, d;
+  int klo_hi, khi_hi;  // accept iff klo_hi < hi(red) < khi_hi
+  int pad[2];
+};
+static_assert(sizeof(RelaxRow) == 48, "relaxed row stride");
+struct RelaxTable {
+  RelaxRow row[8];
+};
+
 template <unsigned MASK, bool SEG>
-__device__ __forceinline__ void stage_table_relaxed(SmemTable* s) {
+__device__ __forceinline__ void stage_table_relaxed(RelaxTable* s) {
   constexpr bool kLo = (MASK & (kSin | kTan)) != 0 || SEG;
   constexpr bool kHi = (MASK & kCos) != 0;
   for (int i = threadIdx.x; i < 8; i += blockDim.x) {
@@ -782,8 +804,14 @@ __device__ __forceinline__ void stage_table_relaxed(SmemTable* s) {
     const Coeffs& c = c_table.seg[k];
     const int klo = i >= 6 ? 0x7fffffff : i == 0 ? (kLo ? kHiRelaxLo : -1) : __double2hiint(c_table.knots[k]);
     const int khi = i >= 6 ? 0 : i == 5 ? (kHi ? kHiRelaxCos : kHiHalfPi) : __double2hiint(c_table.knots[k + 1]);
-    s->row[i] = SegRow{c.a, c.b, c.c, c.d, c.X, c.Y, c.Z, klo, khi, 0.0, 0.0};
+    s->row[i] = RelaxRow{c.a, c.b, c.c, c.d, klo, khi, {0, 0}};
   }
+}
+
+__device__ __forceinline__ int2 lds_i32x2(unsigned addr) {
+  int2 v;
+  asm("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
 }
 
 struct Out3f {
@@ -794,7 +822,7 @@ struct Out3f {
 __device__ __forceinline__ float xor_f(float v, unsigned bits) { return __uint_as_float(__float_as_uint(v) ^ bits); }
 
 template <int SQ, unsigned MASK, bool SEG>
-__device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const SmemTable& tb, int steps, bool* okp) {
+__device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const RelaxTable& tb, int steps, bool* okp) {
   constexpr bool kS = (MASK & kSin) != 0, kC = (MASK & kCos) != 0, kT = (MASK & kTan) != 0;
   const FastConsts& K = c_fast;
   const double a = fabs(static_cast<double>(xf));
@@ -802,43 +830,32 @@ __device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const SmemTable
   const double d = __fma_rn(-K.pi, __dadd_rn(t, -kRintMagic), a);
   const double red = fabs(d);
   const unsigned g = static_cast<unsigned>(__double2loint(__fma_rz(red, K.twelve_over_pi, K.two52))) & 7u;
-  const unsigned ra = static_cast<unsigned>(__cvta_generic_to_shared(&tb)) + g * kRowBytes;
-  const int4 zq = lds_i32x4(ra + offsetof(SegRow, Z));
+  const unsigned ra = static_cast<unsigned>(__cvta_generic_to_shared(&tb)) + g * sizeof(RelaxRow);
+  const int2 br = lds_i32x2(ra + offsetof(RelaxRow, klo_hi));
   const int h = __double2hiint(d) & 0x7fffffff;
-  bool ok = (fabsf(xf) < kRelaxMaxAbs) & (h > zq.z) & (h < zq.w);
+  bool ok = (fabsf(xf) < kRelaxMaxAbs) & (h > br.x) & (h < br.y);
   if constexpr (kT || SEG) ok = ok & (h != kHiGuard);
   const unsigned modd = static_cast<unsigned>(__double2loint(t)) << 31;  // m odd
   const unsigned dx = static_cast<unsigned>(__double2hiint(d)) ^ __float_as_uint(xf);
+  double ca, cb, cc, cd;
+  lds_f64x2(ra + offsetof(RelaxRow, a), ca, cb);
+  lds_f64x2(ra + offsetof(RelaxRow, c), cc, cd);
+  const double ns = __fma_rn(ca, red, cb);  // sine numerator == tangent numerator
+  const double nc = __fma_rn(cc, red, cd);  // cosine numerator == tangent denominator
   Out3f o{0.0f, 0.0f, 0.0f, 0, 0};
   if constexpr (kS || kC) {
-    double X, Y;
-    lds_f64x2(ra + offsetof(SegRow, X), X, Y);
-    const double rad = __fma_rn(__fma_rn(X, red, Y), red, __hiloint2double(zq.y, zq.x));
-    const double rs = fast_rsqrt<SQ>(rad, steps);
-    if constexpr (kS) {
-      double sa, sb;
-      lds_f64x2(ra + offsetof(SegRow, a), sa, sb);
-      o.s = xor_f(__double2float_rn(__dmul_rn(__fma_rn(sa, red, sb), rs)), (dx ^ modd) & 0x80000000u);
-    }
-    if constexpr (kC) {
-      double sc, sd;
-      lds_f64x2(ra + offsetof(SegRow, c), sc, sd);
-      o.c = xor_f(__double2float_rn(__dmul_rn(__fma_rn(sc, red, sd), rs)), modd);
-    }
+    const double rs = fast_rsqrt<SQ>(__fma_rn(ns, ns, __dmul_rn(nc, nc)), steps);
+    if constexpr (kS) o.s = xor_f(__double2float_rn(__dmul_rn(ns, rs)), (dx ^ modd) & 0x80000000u);
+    if constexpr (kC) o.c = xor_f(__double2float_rn(__dmul_rn(nc, rs)), modd);
   }
   const bool guard = h > kHiGuard;
   if constexpr (kT) {
-    double sa, sb, sc, sd;
-    lds_f64x2(ra + offsetof(SegRow, a), sa, sb);
-    lds_f64x2(ra + offsetof(SegRow, c), sc, sd);
-    const double poly = __fma_rn(sa, red, sb);
-    const double den = __fma_rn(sc, red, sd);
     double v;
     if constexpr (SQ == kExact) {
-      v = __ddiv_rn(poly, den);
+      v = __ddiv_rn(ns, nc);
     } else {
-      const double r = fast_rsqrt<SQ>(den, steps);
-      v = __dmul_rn(__dmul_rn(poly, r), r);
+      const double r = fast_rsqrt<SQ>(nc, steps);
+      v = __dmul_rn(__dmul_rn(ns, r), r);
     }
     const float vf = guard ? __int_as_float(0x7f800000) : __double2float_rn(v);
     o.t = xor_f(vf, dx & 0x80000000u);

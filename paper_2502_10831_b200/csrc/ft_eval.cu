@@ -284,7 +284,7 @@ template <int SQ, unsigned MASK, bool SEG>
 struct RelaxedOp {
   template <typename T>
   static constexpr int kGroup = FT_RELAX_GROUP;
-  const SmemTable* tb;   // relaxed rows
+  const RelaxTable* tb;  // relaxed rows
   const SmemTable* tbx;  // bit-exact rows (fallback)
   int steps;
   __device__ __forceinline__ Out3f operator()(float x) const {
@@ -374,13 +374,14 @@ __global__ void __launch_bounds__(kThreads, (kMinBlocksK2<T, MASK>)) k_taylor(co
 template <int SQ, unsigned MASK, bool SEG>
 __global__ void __launch_bounds__(kThreads, MASK == kTan ? FT_MINB_RELAX_TAN : FT_MINB_RELAX)
     k_proposed_relaxed(const EvalArgs a) {
-  __shared__ SmemTable tb[2];
-  stage_table_relaxed<MASK, SEG>(&tb[0]);
-  stage_table(&tb[1]);
+  __shared__ RelaxTable tb;
+  __shared__ SmemTable tbx;
+  stage_table_relaxed<MASK, SEG>(&tb);
+  stage_table(&tbx);
   pdl_wait();
   __syncthreads();
   using Op = RelaxedOp<SQ, MASK, SEG>;
-  stream_map<float, MASK, SEG, Op, FT_TMA_RELAX != 0>(a, Op{&tb[0], &tb[1], a.steps});
+  stream_map<float, MASK, SEG, Op, FT_TMA_RELAX != 0>(a, Op{&tb, &tbx, a.steps});
 }
 
 template <int NT, unsigned MASK>
@@ -553,20 +554,22 @@ cudaError_t chunked(ft_dtype dt, const EvalArgs& a, F&& launch_one) {
 // (kind 0: bit-exact K1 rows; kind 1..7: relaxed f32 rows for that mask).
 __global__ void k_dump_rows(int kind, SmemTable* out) {
   __shared__ SmemTable tb;
+  __shared__ RelaxTable tr;
   switch (kind) {
-    case 1: stage_table_relaxed<1, false>(&tb); break;
-    case 2: stage_table_relaxed<2, false>(&tb); break;
-    case 3: stage_table_relaxed<3, false>(&tb); break;
-    case 4: stage_table_relaxed<4, false>(&tb); break;
-    case 5: stage_table_relaxed<5, false>(&tb); break;
-    case 6: stage_table_relaxed<6, false>(&tb); break;
-    case 7: stage_table_relaxed<7, false>(&tb); break;
+    case 1: stage_table_relaxed<1, false>(&tr); break;
+    case 2: stage_table_relaxed<2, false>(&tr); break;
+    case 3: stage_table_relaxed<3, false>(&tr); break;
+    case 4: stage_table_relaxed<4, false>(&tr); break;
+    case 5: stage_table_relaxed<5, false>(&tr); break;
+    case 6: stage_table_relaxed<6, false>(&tr); break;
+    case 7: stage_table_relaxed<7, false>(&tr); break;
     default: stage_table(&tb); break;
   }
   __syncthreads();
-  const int4* src = reinterpret_cast<const int4*>(&tb);
+  const int4* src = kind == 0 ? reinterpret_cast<const int4*>(&tb) : reinterpret_cast<const int4*>(&tr);
+  const unsigned n16 = (kind == 0 ? sizeof(SmemTable) : sizeof(RelaxTable)) / 16;
   int4* dst = reinterpret_cast<int4*>(out);
-  for (unsigned i = threadIdx.x; i < sizeof(SmemTable) / 16; i += blockDim.x) dst[i] = src[i];
+  for (unsigned i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
 }
 
 }  // namespace

@@ -305,13 +305,17 @@ ROW_DTYPE = np.dtype([("a", "<f8"), ("b", "<f8"), ("c", "<f8"), ("d", "<f8"), ("
                       ("klo", "<f8"), ("khi", "<f8")])
 
 
+RELAX_ROW_DTYPE = np.dtype([("a", "<f8"), ("b", "<f8"), ("c", "<f8"), ("d", "<f8"),
+                            ("klo_hi", "<i4"), ("khi_hi", "<i4"), ("pad", "<i4", (2,))])
+
+
 def device_rows(kind: int = 0) -> np.ndarray:
-    """The 8 shared-memory rows a K1 block stages (kind 0 bit-exact, 1..7 relaxed
-    f32 rows for that mask), copied out of shared memory by a kernel."""
-    out = np.empty(8, ROW_DTYPE)
-    assert out.nbytes == 640
-    L.check(L.lib().ft_device_rows(kind, out.ctypes.data))
-    return out
+    """The 8 shared-memory rows a K1 block stages (kind 0: bit-exact 80-byte rows;
+    1..7: the relaxed f32 48-byte rows for that mask), copied out by a kernel."""
+    buf = np.zeros(640, np.uint8)
+    L.check(L.lib().ft_device_rows(kind, buf.ctypes.data))
+    dt = ROW_DTYPE if kind == 0 else RELAX_ROW_DTYPE
+    return buf[: 8 * dt.itemsize].view(dt).copy()
 
 
 def release(device: int = -1) -> None:
