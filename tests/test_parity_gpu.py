@@ -563,3 +563,36 @@ def test_concurrent_callers(ft):
     for t in th:
         t.join(timeout=300)
     assert not errors, errors
+
+
+def test_device_tables_read_back_bitwise(ft):
+    """the constant tables as the GPU holds them -- the __constant__
+    copy of every translation unit and the shared-memory rows the K1 kernels
+    stage (bit-exact and relaxed), copied out by a kernel -- carry the reference's
+    segment_table bits (R:segments.hpp:33-66) and the documented brackets."""
+    ref = O.segment_table("ref" if O.ref_available() else "port")
+    for unit in range(4):
+        assert same_bits(ft.device_const_table(unit), ref), unit
+    coef = ref[:42].reshape(6, 7)
+    knots = ref[42:]
+    hi = lambda v: int(np.int64(np.float64(v).view(np.int64)) >> 32)  # noqa: E731
+    rows = ft.device_rows(0)
+    for i in range(8):
+        k = min(i, 5)
+        got = np.array([rows[i][f] for f in ("a", "b", "c", "d", "X", "Y", "Z")])
+        assert same_bits(got, coef[k]), i
+        klo = hi(2.0**-17) if i == 0 else 0 if i >= 6 else hi(knots[k])
+        khi = hi(0.5 * math.pi) if i == 5 else 0 if i >= 6 else hi(knots[k + 1])
+        assert (int(rows[i]["klo_hi"]), int(rows[i]["khi_hi"])) == (klo, khi), i
+    for mask in range(1, 8):
+        rr = ft.device_rows(mask)
+        for i in range(8):
+            k = min(i, 5)
+            got = np.array([rr[i][f] for f in ("a", "b", "c", "d")])
+            assert same_bits(got, coef[k][:4]), (mask, i)
+            lo_needed = bool(mask & 5)
+            cos_in = bool(mask & 2)
+            klo = 0x7FFFFFFF if i >= 6 else (hi(2.0**-11) if lo_needed else -1) if i == 0 else hi(knots[k])
+            khi = 0 if i >= 6 else (hi(0.5 * math.pi - 2.0**-11) if cos_in else hi(0.5 * math.pi)) if i == 5 \
+                else hi(knots[k + 1])
+            assert (int(rr[i]["klo_hi"]), int(rr[i]["khi_hi"])) == (klo, khi), (mask, i)
