@@ -280,10 +280,13 @@ struct TaylorOp {
 #ifndef FT_RELAX_GROUP
 #define FT_RELAX_GROUP 1  // elements per exact-path branch in the relaxed kernels
 #endif
+#ifndef FT_RELAX_GROUP_TAN
+#define FT_RELAX_GROUP_TAN 1  // the same for the tan-only relaxed kernels
+#endif
 template <int SQ, unsigned MASK, bool SEG>
 struct RelaxedOp {
   template <typename T>
-  static constexpr int kGroup = FT_RELAX_GROUP;
+  static constexpr int kGroup = MASK == kTan ? FT_RELAX_GROUP_TAN : FT_RELAX_GROUP;
   const RelaxTable* tb;  // relaxed rows
   const SmemTable* tbx;  // bit-exact rows (fallback)
   int steps;
