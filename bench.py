@@ -20,8 +20,10 @@ array -- strong-scaled (N=1: all 2^33 elements on one GPU; N>1: 2^33/N each).
 
 One step = one K1/K2 launch sequence over the shard (inputs already resident in
 HBM).  L2: the headline's x + outputs are 8 GiB per GPU (>> 126 MB L2), no
-flush; configs whose input is smaller than L2 (cfg1) are timed step by step
-with a 2x-L2 flush between steps (outside the timed pairs).  Timing: CUDA
+flush; configs whose input is smaller than L2 (cfg1: 64 MiB) rotate the timed
+steps over identical copies of the batch in distinct buffers, so that >= 2x L2
+of other traffic separates two reads of one x (every step reads x from HBM,
+with no flush kernel and its dirty-line write-back inside the timing).  Timing: CUDA
 events on the launching stream, barrier + synchronize on both sides, max over
 ranks.
 
@@ -251,22 +253,31 @@ def plan(w, world: int, rank: int, elements: int = 0):
     return n, rank * n, "weak", n * world
 
 
-def config_dict(w, n: int, world: int, policy: str, flush: bool) -> dict:
+def config_dict(w, n: int, world: int, policy: str, rotate: int) -> dict:
     """The `config` object of a line: identical for our arm and the reference arm."""
     names = [nm for j, nm in enumerate(("sin", "cos", "tan")) if w.mask & (1 << j)]
+    step_bytes = w.bytes_per_elem * n
     d = {"workload": w.name, "description": w.note, "elements_per_gpu": n, "outputs": names,
          "sqrt_mode": "fisr(1) (SqrtMode{} default)" if w.kind == 0 else f"Taylor-{w.n_terms}",
          "parallelism": f"dp{world} contiguous shards, no data exchange",
-         "l2": (f"x ({w.itemsize * n / 2**20:.0f} MiB) smaller than L2: 2x-L2 flush between timed steps"
-                if flush else f"inputs larger than L2 (x + outputs = {w.bytes_per_elem * n / 2**30:.1f} GiB "
-                              "per GPU vs 126 MB L2); no flush")}
+         "l2": (f"x ({w.itemsize * n / 2**20:.0f} MiB) smaller than L2: timed steps rotate over {rotate} "
+                f"copies of the batch (x + outputs = {rotate * step_bytes / 2**20:.0f} MiB, "
+                f"{rotate * step_bytes / L2_BYTES:.1f}x L2), so every step reads its x from HBM; no flush"
+                if rotate > 1 else f"inputs larger than L2 (x + outputs = {step_bytes / 2**30:.1f} GiB "
+                                   "per GPU vs 126 MB L2); no flush")}
     if w.itemsize == 4:
         d["f32_policy"] = policy
     return d
 
 
-def needs_flush(w, n: int) -> bool:
-    return w.itemsize * n < L2_BYTES
+def rotation(w, n: int) -> int:
+    """Buffer sets the timed steps cycle through: 1 when x alone exceeds L2, else
+    enough copies that the other sets' traffic between two uses of one set is
+    >= 2x L2 (x is then evicted before it is read again)."""
+    if w.itemsize * n >= L2_BYTES:
+        return 1
+    step = w.bytes_per_elem * n
+    return 1 + max(2, -(-2 * L2_BYTES // step))
 
 
 # ------------------------------------------------------------------ reference arm
@@ -311,7 +322,7 @@ def run_reference(args) -> None:
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64" if w.itemsize == 8 else "f32", "data": "synthetic",
-        "config": config_dict(w, n_cfg, args.gpus, args.f32_policy, needs_flush(w, n_cfg)),
+        "config": config_dict(w, n_cfg, args.gpus, args.f32_policy, rotation(w, n_cfg)),
         "cpu_baseline": {"value": round(value, 6), "unit": "Gelem/s", "cores": threads,
                          "kind": kind, "sample": sample, "elements_per_step": n,
                          "api_batch_single_thread_gelem_s": api_single_thread_rate(w)},
@@ -369,29 +380,18 @@ class Ctx:
         return float(t.item())
 
 
-def time_steps(step, k: int, stream, flush: bool) -> float:
-    """Mean device time of one step (ms) over k steps, CUDA events on `stream`.
-    flush: a 2x-L2 write before every step, outside the timed event pairs."""
+def time_steps(step, k: int, stream) -> float:
+    """Mean device time of one step (ms) over k back-to-back steps, CUDA events
+    on `stream`; step(i) runs the i-th step."""
     import torch
 
-    import paper_2502_10831_b200 as ft
-
-    if not flush:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(k):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / k
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
-    for a, b in evs:
-        ft.l2_flush()
-        a.record(stream)
-        step()
-        b.record(stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(k):
+        step(i)
+    e1.record(stream)
     torch.cuda.synchronize()
-    return sum(a.elapsed_time(b) for a, b in evs) / k
+    return e0.elapsed_time(e1) / k
 
 
 def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0, keep: bool = False):
@@ -409,13 +409,16 @@ def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0
     names = [nm for j, nm in enumerate(("sin", "cos", "tan")) if w.mask & (1 << j)]
     out = {nm: torch.empty_like(x) for nm in names}
     mode = ft.SqrtMode()
-    flush = needs_flush(w, n)
+    rot = rotation(w, n)
+    # identical copies of the batch in distinct buffers (see rotation())
+    sets = [(x, out)] + [(x.clone(), {nm: torch.empty_like(x) for nm in names}) for _ in range(rot - 1)]
 
-    def step():
+    def step(i=0):
+        xi, oi = sets[i % rot]
         if w.kind == 0:
-            ft.proposed_eval(x, w.mask, mode, out=out)
+            ft.proposed_eval(xi, w.mask, mode, out=oi)
         else:
-            ft.taylor_eval(x, w.n_terms, w.mask, out=out)
+            ft.taylor_eval(xi, w.n_terms, w.mask, out=oi)
 
     with ft.f32_policy(policy):
         clocks = ClockSampler(ctx.device_index)  # samples from warm-up start to timed-region end
@@ -427,9 +430,9 @@ def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0
         ctx.barrier()
         torch.cuda.synchronize()
         l0 = ft.launch_count()
-        ms_local = time_steps(step, steps, stream, flush)
+        ms_local = time_steps(step, steps, stream)
         ctx.barrier()
-        launches = ft.launch_count() - l0 - (steps if flush else 0)
+        launches = ft.launch_count() - l0
         clk = clocks.stop()
     ms = ctx.max_over_ranks(ms_local)
     value = total / (ms / 1e3) / 1e9
@@ -460,10 +463,11 @@ def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0
     entry = {"value": round(value, 4), "unit": "Gelem/s", "per_gpu_gelem_s": round(n / (ms / 1e3) / 1e9, 4),
              "ms_per_step": round(ms, 5), "steps": steps, "warmup": max(warmup, 3), "scaling": scaling,
              "dtype": "f64" if w.itemsize == 8 else "f32",
-             "config": config_dict(w, n, ctx.world, policy, flush), "roofline": roofline,
+             "config": config_dict(w, n, ctx.world, policy, rot), "roofline": roofline,
              "fp64_roof": fp64_roof(w.name, n / (ms_local / 1e3) / 1e9), "gpu_launches": int(launches),
              "clocks": clk, "accuracy": accuracy}
     state = {"x": x, "out": out, "n": n, "names": names, "tdt": tdt} if keep else None
+    del sets
     if not keep:
         del x, out
         torch.cuda.empty_cache()

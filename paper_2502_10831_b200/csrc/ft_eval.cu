@@ -277,6 +277,9 @@ struct TaylorOp {
 
 // Relaxed f32 proposed path (ft_core.cuh: relaxed_proposed_core): certified
 // lanes within 2 ulp of the reference, the rest redone bit-exactly.
+#ifndef FT_NULL_EVAL
+#define FT_NULL_EVAL 0  // 1: tools-only build whose relaxed kernels copy x (roofline of the loop itself)
+#endif
 #ifndef FT_RELAX_GROUP
 #define FT_RELAX_GROUP 1  // elements per exact-path branch in the relaxed kernels
 #endif
@@ -291,6 +294,9 @@ struct RelaxedOp {
   const SmemTable* tbx;  // bit-exact rows (fallback)
   int steps;
   __device__ __forceinline__ Out3f operator()(float x) const {
+#if FT_NULL_EVAL
+    return Out3f{x, x, x, 0, 0};  // measurement-only build: the kernel's traffic without its math
+#endif
     bool ok;
     Out3f o = relaxed_proposed_core<SQ, MASK, SEG>(x, *tb, steps, &ok);
     if (!ok) o = relaxed_slow<SQ, MASK, SEG>(x, tbx, steps);  // rare

@@ -72,5 +72,5 @@ def test_our_arm_line():
         assert 0 < c["roofline"]["frac"] < 1.2
         assert c["accuracy"]["over_2ulp"] == [0, 0, 0] and max(c["accuracy"]["max_ulp_vs_oracle"]) <= 2
         assert c["config"]["f32_policy"] == "ulp2"
-    assert "flush" in d["configs"]["cfg1"]["config"]["l2"]
+    assert "rotate over 3 copies" in d["configs"]["cfg1"]["config"]["l2"]
     assert d["configs"]["cfg1"]["gpu_launches"] == 2000
