@@ -27,6 +27,9 @@ with no flush kernel and its dirty-line write-back inside the timing).  Timing: 
 events on the launching stream, barrier + synchronize on both sides, max over
 ranks.
 
+`sustained` repeats the headline step for ~20 s of device time (the
+power-capped steady state; the headline window is under a second).
+
 `e2e` is the headline metric through the public host-pointer C-ABI call
 (ft_proposed_batch_host) with pinned host buffers over the full shard: every
 step copies x in and sin/cos/tan out.  `e2e_variants` adds the reference-shaped
@@ -466,12 +469,47 @@ def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0
              "config": config_dict(w, n, ctx.world, policy, rot), "roofline": roofline,
              "fp64_roof": fp64_roof(w.name, n / (ms_local / 1e3) / 1e9), "gpu_launches": int(launches),
              "clocks": clk, "accuracy": accuracy}
-    state = {"x": x, "out": out, "n": n, "names": names, "tdt": tdt} if keep else None
+    state = {"x": x, "out": out, "n": n, "total": total, "names": names, "tdt": tdt} if keep else None
     del sets
     if not keep:
         del x, out
         torch.cuda.empty_cache()
     return entry, state
+
+
+def sustained(ctx: Ctx, w, state, seconds: float, ms_hint: float, policy: str) -> dict:
+    """The headline step repeated back to back for ~`seconds` of device time on
+    the same buffers (the power-capped steady state a long production batch
+    sees, next to the short headline window)."""
+    import torch
+
+    import paper_2502_10831_b200 as ft
+
+    x, out = state["x"], state["out"]
+    mode = ft.SqrtMode()
+    k = max(10, int(seconds * 1e3 / max(ms_hint, 1e-3)))
+
+    def step(i=0):
+        if w.kind == 0:
+            ft.proposed_eval(x, w.mask, mode, out=out)
+        else:
+            ft.taylor_eval(x, w.n_terms, w.mask, out=out)
+
+    with ft.f32_policy(policy):
+        clocks = ClockSampler(ctx.device_index)
+        clocks.start()
+        clocks.mark()
+        torch.cuda.synchronize()
+        ctx.barrier()
+        ms_local = time_steps(step, k, torch.cuda.current_stream())
+        ctx.barrier()
+        clk = clocks.stop()
+    ms = ctx.max_over_ranks(ms_local)
+    n, total = state["n"], state["total"]
+    peak, _ = peaks()
+    return {"value": round(total / (ms / 1e3) / 1e9, 4), "unit": "Gelem/s", "ms_per_step": round(ms, 5),
+            "steps": k, "seconds": round(k * ms / 1e3, 2),
+            "roofline_frac": round(w.bytes_per_elem * n / (ms_local / 1e3) / 1e9 / peak, 4), "clocks": clk}
 
 
 def e2e_pinned(ctx: Ctx, w, state, steps: int, n_e2e: int) -> dict:
@@ -565,9 +603,14 @@ def run_ours(args) -> None:
     w = CONFIGS[args.config]
     head, state = measure(ctx, w, args.steps, args.warmup, args.f32_policy, args.elements, keep=True)
 
+    sus = None
+    if args.sustained_seconds > 0:
+        sus = sustained(ctx, w, state, args.sustained_seconds, head["ms_per_step"], args.f32_policy)
+
     e2e, e2e_var = None, None
     if not args.no_e2e:
-        n_e2e = min(state["n"], args.e2e_elements or state["n"])
+        # the whole shard at N=1; 2^26 per rank at N>1 (N ranks pin N x 2-8 GiB of host memory)
+        n_e2e = min(state["n"], args.e2e_elements or (state["n"] if ctx.world == 1 else 1 << 26))
         e2e = e2e_pinned(ctx, w, state, args.e2e_steps, n_e2e)
         e2e_var = e2e_pageable(ctx, w, state, args.e2e_steps, n_e2e) or None
 
@@ -609,7 +652,8 @@ def run_ours(args) -> None:
             "dtype": head["dtype"], "data": "synthetic", "config": head["config"],
             "per_gpu_gelem_s": head["per_gpu_gelem_s"], "roofline": head["roofline"],
             "fp64_roof": head["fp64_roof"], "cpu_baseline": cpu, "e2e": e2e, "e2e_variants": e2e_var,
-            "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "accuracy": head["accuracy"],
+            "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "sustained": sus,
+            "accuracy": head["accuracy"],
             "configs": extra or None,
         }
         print(json.dumps(line), flush=True)
@@ -635,6 +679,8 @@ def main() -> None:
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="process-group backend; gloo only for tests that run several ranks on one GPU")
     ap.add_argument("--f32-policy", choices=["ulp2", "bitwise"], default="ulp2")
+    ap.add_argument("--sustained-seconds", type=float, default=20.0,
+                    help="also run the headline step back to back for this long (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-elements", type=int, default=0,
                     help="elements per rank per e2e step (default: the whole shard)")

@@ -51,7 +51,7 @@ def test_reference_sample_is_deterministic():
 @pytest.mark.gpu
 def test_our_arm_line():
     d = run_bench("--steps", "20", "--warmup", "3", "--e2e-elements", str(1 << 22), "--e2e-steps", "2",
-                  "--configs", "cfg1,cfg3,cfg4_f32")
+                  "--configs", "cfg1,cfg3,cfg4_f32", "--sustained-seconds", "2")
     assert BASE_KEYS <= set(d) and "roofline" in d and "clocks" in d
     assert d["n_gpus"] == 1 and d["scaling"] == "weak" and d["dtype"] == "f64"
     assert d["gpu_launches"] == 20
@@ -63,6 +63,8 @@ def test_our_arm_line():
     assert d["accuracy"]["max_ulp_vs_oracle"] == [0, 0, 0]
     assert d["accuracy"]["bit_mismatch_vs_oracle"] == [0, 0, 0]
     assert d["cpu_baseline"]["value"] > 0
+    su = d["sustained"]
+    assert su["value"] > 0 and su["seconds"] >= 1.5 and "sm_mhz" in su["clocks"]
     ev = d["e2e_variants"]
     assert set(ev) == {"api_single_output_x3_pageable", "fused_pageable"}
     assert all(v["value"] > 0 for v in ev.values())

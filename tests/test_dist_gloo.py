@@ -156,7 +156,7 @@ def test_bench_two_ranks_real_k3_stats_equal_one_rank():
     from conftest import ROOT
 
     common = ["--config", "cfg5", "--elements", str(1 << 30), "--configs", "none", "--no-e2e", "--no-cpu",
-              "--steps", "3", "--warmup", "3", "--f32-policy", "bitwise"]
+              "--steps", "3", "--warmup", "3", "--f32-policy", "bitwise", "--sustained-seconds", "0"]
     two = _bench_json([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                        "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
                        os.path.join(ROOT, "bench.py"), "--gpus", "2", "--backend", "gloo", *common])
@@ -169,7 +169,8 @@ def test_bench_two_ranks_real_k3_stats_equal_one_rank():
         assert a2[k] == a1[k], k
     assert a1["checked"] == 1 << 30 and a1["max_ulp_vs_oracle"] == [0, 0, 0]
     full = _bench_json([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "cfg5", "--configs", "none",
-                        "--no-e2e", "--no-cpu", "--steps", "2", "--warmup", "3", "--f32-policy", "bitwise"])
+                        "--no-e2e", "--no-cpu", "--steps", "2", "--warmup", "3", "--f32-policy", "bitwise",
+                        "--sustained-seconds", "0"])
     assert full["accuracy"]["checked"] == 1 << 33
     # profiles/r01e_cfg5_full.json (round 1, bit-exact kernel)
     assert full["accuracy"]["checksum"] == [18298921530744543647, 18299087910619986952, 18375888137372184031]

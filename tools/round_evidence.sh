@@ -9,12 +9,12 @@ out=gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()" > $out/${tag}_smoke.log 2>&1; echo "smoke rc=$?"
 python bench.py > $out/${tag}_bench.json 2> $out/${tag}_bench.err; echo "bench rc=$?"
 # launch lists (cold-cache, serialised: shares, not absolutes)
-python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --configs none > $out/${tag}_plain.log 2>&1 && \
+python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --sustained-seconds 0 --configs none > $out/${tag}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/${tag}_launches.csv \
-    python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --configs none > $out/${tag}_ncu_launch.log 2>&1
-python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --config-steps 5 > $out/${tag}_plain_cfgs.log 2>&1 && \
+    python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --sustained-seconds 0 --configs none > $out/${tag}_ncu_launch.log 2>&1
+python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --sustained-seconds 0 --config-steps 5 > $out/${tag}_plain_cfgs.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/${tag}_launches_configs.csv \
-    python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --config-steps 5 > $out/${tag}_ncu_launch_cfgs.log 2>&1
+    python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --sustained-seconds 0 --config-steps 5 > $out/${tag}_ncu_launch_cfgs.log 2>&1
 echo "launches rc=$?"
 # full captures of the dominant kernel of every workload
 for spec in "k1_cfg2:k_proposed:cfg2" "k1r_cfg1:k_proposed:cfg1" "k1r_cfg3:k_proposed:cfg3" "k1r_cfg5:k_proposed:cfg5" \
