@@ -313,3 +313,40 @@ def test_relaxed_guard_bucket_margin():
     lo = (np.uint64(b >> 32 << 32)).view(np.float64)
     hi = (np.uint64((b >> 32 << 32) | 0xFFFFFFFF)).view(np.float64)
     assert g - lo > 2.3e-7 and hi - g > 2.3e-7
+
+
+def test_new_entry_points_validate_without_gpu(ft):
+    """Round-2 ABI additions reject bad arguments before touching CUDA, and the
+    f32 policy round-trips (process-wide)."""
+    from paper_2502_10831_b200 import _lib
+
+    L = _lib.lib()
+    assert L.ft_device_rows(9, C.c_void_p(16)) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_device_rows(0, None) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_device_const_table(7, C.c_void_p(16)) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_device_const_table(0, None) == _lib.FT_ERR_INVALID_ARG
+    assert L.ft_set_f32_policy(2) == _lib.FT_ERR_INVALID_ARG
+    assert b"policy" in L.ft_last_error_string()
+    assert ft.get_f32_policy() == "ulp2"  # default
+    with ft.f32_policy("bitwise"):
+        assert ft.get_f32_policy() == "bitwise" and L.ft_get_f32_policy() == _lib.FT_F32_BITWISE
+    assert ft.get_f32_policy() == "ulp2"
+    # without a visible device ft_release reports the CUDA error instead of crashing
+    rc = L.ft_release(-1)
+    assert rc in (_lib.FT_OK, _lib.FT_ERR_NO_DEVICE, _lib.FT_ERR_CUDA)
+
+
+def test_python_outputs_are_validated(ft):
+    """caller-supplied host outputs of the wrong dtype, size or layout
+    are rejected before any pointer reaches the C ABI."""
+    x = np.zeros(16, np.float64)
+    with pytest.raises(TypeError):
+        ft.proposed_batch(x, 1, out={"sin": np.zeros(16, np.float32)})
+    with pytest.raises(ValueError):
+        ft.proposed_batch(x, 1, out={"sin": np.zeros(8, np.float64)})
+    with pytest.raises(ValueError):
+        ft.proposed_batch(x, 1, out={"sin": np.zeros(32, np.float64)[::2]})
+    with pytest.raises(TypeError):
+        ft.proposed_batch(x, 3, out={"sin": np.zeros(16, np.float64)})  # cos missing
+    with pytest.raises(ValueError):
+        ft.proposed_batch(x, 0)
