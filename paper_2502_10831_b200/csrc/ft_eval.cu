@@ -51,6 +51,12 @@ constexpr int kMinBlocksK2 =
 #ifndef FT_BATCH_SLOW
 #define FT_BATCH_SLOW 1
 #endif
+#ifndef FT_PINGPONG
+#define FT_PINGPONG 0  // 1: per-thread loop unrolled by two with ping-pong prefetch registers (r02r: -3%)
+#endif
+#ifndef FT_ADDR32
+#define FT_ADDR32 1
+#endif
 #ifndef FT_RPF
 #define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
 #endif
@@ -95,6 +101,25 @@ __device__ __forceinline__ void bulk_wait_read_1() {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Cache hints of the per-thread streaming accesses (experiments: FT_LD_CS=0
+// plain loads, FT_ST_CS=0 plain write-back stores).
+#ifndef FT_LD_CS
+#define FT_LD_CS 1
+#endif
+#ifndef FT_ST_CS
+#define FT_ST_CS 1
+#endif
+template <typename V>
+__device__ __forceinline__ V ld_x(const V* p) {
+  if constexpr (FT_LD_CS) return __ldcs(p);
+  else return __ldg(p);
+}
+template <typename V>
+__device__ __forceinline__ void st_out(V* p, const V& v) {
+  if constexpr (FT_ST_CS) __stcs(p, v);
+  else *p = v;
 }
 
 // The streaming map shared by every evaluation kernel.  `op(T) -> Out3` (or
@@ -174,9 +199,9 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
     auto body = [&](const VT& xin, unsigned v) {
       VT res[3];
       compute(xin, v, res);
-      if constexpr ((MASK & kSin) != 0) __stcs(reinterpret_cast<VT*>(o0) + v, res[0]);
-      if constexpr ((MASK & kCos) != 0) __stcs(reinterpret_cast<VT*>(o1) + v, res[1]);
-      if constexpr ((MASK & kTan) != 0) __stcs(reinterpret_cast<VT*>(o2) + v, res[2]);
+      if constexpr ((MASK & kSin) != 0) st_out(reinterpret_cast<VT*>(o0) + v, res[0]);
+      if constexpr ((MASK & kCos) != 0) st_out(reinterpret_cast<VT*>(o1) + v, res[1]);
+      if constexpr ((MASK & kTan) != 0) st_out(reinterpret_cast<VT*>(o2) + v, res[2]);
     };
     if constexpr (TMA && !SEG) {
       // Block tiles of kThreads vectors; x register-prefetched one tile ahead;
@@ -221,14 +246,52 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
     // overlaps the arithmetic.  With 4 blocks/SM (<= 64 registers) this beat
     // direct loads, cp.async / TMA staging, L2 prefetch hints and prefetching
     // two iterations ahead (profiles/r01_k1_variants.json).
+#if FT_RPF == 2
+    VT cur{}, nx1{};
+    if (tid < nv) cur = ld_x(xv + tid);
+    if (tid + stride < nv) nx1 = ld_x(xv + tid + stride);
+    for (unsigned v = tid; v < nv; v += stride) {
+      VT nx2{};
+      if (v + 2 * stride < nv) nx2 = ld_x(xv + v + 2 * stride);
+      body(cur, v);
+      cur = nx1;
+      nx1 = nx2;
+    }
+#elif FT_PINGPONG
+    // Unrolled by two with ping-pong registers: no register moves between
+    // iterations, and the prefetch index is clamped to the last vector instead
+    // of predicated (the extra load of a thread's final round is discarded).
+    // Indices stay 32-bit so each address is one IMAD.WIDE.U32.
+    if (nv > 0) {
+      const unsigned last = nv - 1;
+      VT cur = ld_x(xv + min(tid, last));
+      unsigned v = tid;
+      while (v < nv) {
+        const unsigned v1 = v + stride;
+        const VT nxt = ld_x(xv + min(v1, last));
+        body(cur, v);
+        if (v1 >= nv) break;
+        const unsigned v2 = v1 + stride;
+        cur = ld_x(xv + min(v2, last));
+        body(nxt, v1);
+        v = v2;
+      }
+    }
+#else
     VT cur{};
-    if (tid < nv) cur = __ldcs(xv + tid);
+    if (tid < nv) cur = ld_x(xv + tid);
     for (unsigned v = tid; v < nv; v += stride) {
       VT nxt{};
-      if (v + stride < nv) nxt = __ldcs(xv + v + stride);
+#if FT_ADDR32
+      const unsigned vn = v + stride;  // 32-bit index: one IMAD.WIDE.U32 per address
+      if (vn < nv) nxt = ld_x(xv + vn);
+#else
+      if (v + stride < nv) nxt = ld_x(xv + v + stride);
+#endif
       body(cur, v);
       cur = nxt;
     }
+#endif
 #else
     for (unsigned v = tid; v < nv; v += stride) body(__ldcs(xv + v), v);
 #endif

@@ -22,7 +22,11 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-MODES = {"fisr1": (1, 1), "exact": (0, 0)}
+MODES = {"fisr1": (1, 1), "exact": (0, 0), "fisr2": (1, 2), "fisr0": (1, 0), "fisr3": (1, 3)}
+# every mask in the default mode and exact; the other sqrt modes (unrolled fisr(2),
+# the runtime-step kernel for fisr(0) / fisr(3)) on the fused mask
+CASES = ([(m, "fisr1") for m in (7, 3, 4, 1, 2, 5, 6)] + [(m, "exact") for m in (7, 3, 4)]
+         + [(7, "fisr2"), (7, "fisr0"), (7, "fisr3")])
 CHUNK = 1 << 28
 ALL = 1 << 32
 
@@ -39,11 +43,8 @@ def _stats_buf():
     return torch.zeros(312, dtype=torch.uint8, device="cuda")
 
 
-@pytest.mark.parametrize("mode", list(MODES))
-@pytest.mark.parametrize("mask", [7, 3, 4, 1, 2, 5, 6])
+@pytest.mark.parametrize("mask,mode", CASES)
 def test_every_float_relaxed_within_2ulp_same_segments(ft, mask, mode):
-    if mode == "exact" and mask not in (7, 3, 4):
-        pytest.skip("exact mode: masks 7, 3, 4")
     sm = ft.SqrtMode(*MODES[mode])
     buf = _stats_buf()
     max_ulp, over, seg_mm, checked = [0, 0, 0], [0, 0, 0], [0, 0], 0
