@@ -214,11 +214,16 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
       const unsigned nt = nv / kThreads;
       unsigned t = blockIdx.x;
       VT cur{};
-      if (t < nt) cur = __ldcs(xv + t * kThreads + threadIdx.x);
+      if (t < nt) cur = __ldcs(xv + (t * kThreads + threadIdx.x));
       unsigned slot = 0;
       for (; t < nt; t += gridDim.x, slot = slot == 2 ? 0 : slot + 1) {
         VT nxt{};
+#if FT_ADDR32
+        // 32-bit element index, one IMAD.WIDE.U32 for the address
+        if (t + gridDim.x < nt) nxt = __ldcs(xv + ((t + gridDim.x) * kThreads + threadIdx.x));
+#else
         if (t + gridDim.x < nt) nxt = __ldcs(xv + (t + gridDim.x) * kThreads + threadIdx.x);
+#endif
         VT res[3];
         compute(cur, t * kThreads + threadIdx.x, res);
         cur = nxt;
