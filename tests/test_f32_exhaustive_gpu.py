@@ -147,3 +147,56 @@ def test_every_float_vs_reference_library(ft, policy):
         assert tot["n_bit_mismatch"] == [0, 0, 0] and tot["max_ulp"] == [0, 0, 0]
     else:
         assert max(tot["max_ulp"]) <= 2
+
+
+def _ulp32(a: np.ndarray, b: np.ndarray) -> int:
+    ia, ib = a.view(np.int32).astype(np.int64), b.view(np.int32).astype(np.int64)
+    oa = np.where(ia < 0, -(ia & 0x7FFFFFFF), ia)
+    ob = np.where(ib < 0, -(ib & 0x7FFFFFFF), ib)
+    na, nb = np.isnan(a), np.isnan(b)
+    d = np.abs(oa - ob)
+    d[na & nb] = 0
+    d[na ^ nb] = 1 << 40
+    return int(d.max()) if d.size else 0
+
+
+@pytest.mark.parametrize("mask", range(1, 8))
+def test_relaxed_ragged_misaligned_every_mask(ft, mask):
+    """The default-policy f32 kernels on offset views (unaligned pointers -> the
+    scalar tail path) and ragged sizes: within 2 ulp of the oracle and equal to
+    the aligned vectorised run of the same elements."""
+    rng = np.random.default_rng(100 + mask)
+    base = rng.uniform(-3e3, 3e3, 70001).astype(np.float32)
+    full = ft.proposed_eval(torch.from_numpy(base).cuda(), mask)
+    for off in (0, 1, 3):
+        for n in (1, 2, 3, 5, 17, 1023, 4097, 70001 - off):
+            xd = torch.from_numpy(base).cuda()[off:off + n]
+            out = {nm: torch.empty(n + 1, dtype=torch.float32, device="cuda")[1:n + 1]
+                   for j, nm in enumerate(("sin", "cos", "tan")) if mask & (1 << j)}
+            ft.proposed_eval(xd, mask, out=out)
+            torch.cuda.synchronize()
+            ref = O.proposed(base[off:off + n], mask)
+            for f in out:
+                g = out[f].cpu().numpy()
+                assert _ulp32(g, ref[f]) <= 2, (off, n, f)
+                assert np.array_equal(g.view(np.uint32), full[f][off:off + n].cpu().numpy().view(np.uint32))
+
+
+def test_relaxed_golden_vectors_and_segments(ft, golden):
+    """Every f32 golden vector (edge cases, knots +- ulps, quadrant edges, pole
+    guard, +-0, huge, non-finite) in every SqrtMode of the fixture: within 2 ulp
+    of the reference's outputs and the identical segment choices."""
+    from conftest import MODES as GM, golden_cases
+
+    n = 0
+    for case, mode, x, ref in golden_cases(golden):
+        if x.dtype != np.float32:
+            continue
+        out = ft.proposed_eval(torch.from_numpy(x).cuda(), 7, ft.SqrtMode(*GM[mode]), seg=True)
+        torch.cuda.synchronize()
+        for f in ("sin", "cos", "tan"):
+            assert _ulp32(out[f].cpu().numpy(), ref[f]) <= 2, (case, mode, f)
+        assert np.array_equal(out["seg_sc"].cpu().numpy(), ref["seg_sc"]), (case, mode)
+        assert np.array_equal(out["seg_t"].cpu().numpy(), ref["seg_t"]), (case, mode)
+        n += x.size
+    assert n > 5000
