@@ -76,3 +76,24 @@ def test_our_arm_line():
         assert c["config"]["f32_policy"] == "ulp2"
     assert "rotate over 3 copies" in d["configs"]["cfg1"]["config"]["l2"]
     assert d["configs"]["cfg1"]["gpu_launches"] == 2000
+
+
+def test_plan_shards_weak_and_strong():
+    """bench.plan: cfg5 is one fixed 2^33 array split contiguously over the ranks
+    (strong); every other config gives each rank its own shard (weak)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2502_10831_b200.configs import CONFIGS
+
+    w5 = CONFIGS["cfg5"]
+    spans = [bench.plan(w5, 8, r) for r in range(8)]
+    assert all(s[2] == "strong" and s[3] == 1 << 33 and s[0] == 1 << 30 for s in spans)
+    assert [s[1] for s in spans] == [r << 30 for r in range(8)]
+    n, lo, scaling, total = bench.plan(CONFIGS["cfg2"], 4, 3)
+    assert (n, lo, scaling, total) == (1 << 28, 3 << 28, "weak", 1 << 30)
+    assert bench.plan(w5, 2, 1, elements=1 << 30) == (1 << 29, 1 << 29, "strong", 1 << 30)
+    # only cfg1's input fits in L2: rotate over 3 copies
+    assert {c: bench.rotation(w, w.n) for c, w in CONFIGS.items()} == {
+        "cfg1": 3, "cfg2": 1, "cfg3": 1, "cfg4_f32": 1, "cfg4_f64": 1, "cfg5": 1}
+    d = bench.config_dict(CONFIGS["cfg1"], 1 << 24, 1, "ulp2", 3)
+    assert d["f32_policy"] == "ulp2" and "rotate over 3 copies" in d["l2"]
