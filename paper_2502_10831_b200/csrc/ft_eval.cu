@@ -57,6 +57,9 @@ constexpr int kMinBlocksK2 =
 #ifndef FT_ADDR32
 #define FT_ADDR32 1
 #endif
+#ifndef FT_L2PF
+#define FT_L2PF 0  // >0: also prefetch x into L2 this many iterations ahead (per-thread loop)
+#endif
 #ifndef FT_RPF
 #define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
 #endif
@@ -290,6 +293,12 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
 #if FT_ADDR32
       const unsigned vn = v + stride;  // 32-bit index: one IMAD.WIDE.U32 per address
       if (vn < nv) nxt = ld_x(xv + vn);
+#if FT_L2PF > 0
+      // DRAM -> L2 prefetch FT_L2PF iterations ahead (no register held), so the
+      // one-ahead register load hits L2
+      const unsigned vp = v + FT_L2PF * stride;
+      if (vp < nv) asm volatile("prefetch.global.L2 [%0];" ::"l"(xv + vp));
+#endif
 #else
       if (v + stride < nv) nxt = ld_x(xv + v + stride);
 #endif
