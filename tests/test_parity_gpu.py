@@ -596,3 +596,37 @@ def test_device_tables_read_back_bitwise(ft):
             khi = 0 if i >= 6 else (hi(0.5 * math.pi - 2.0**-11) if cos_in else hi(0.5 * math.pi)) if i == 5 \
                 else hi(knots[k + 1])
             assert (int(rr[i]["klo_hi"]), int(rr[i]["khi_hi"])) == (klo, khi), (mask, i)
+
+
+def test_launches_capture_into_cuda_graph(ft):
+    """The K1/K2 launches (cudaLaunchKernelEx with programmatic dependent launch)
+    are stream-capturable: a CUDA graph of fused proposed + Taylor steps replays
+    to the same bits as eager launches."""
+    w = CONFIGS["cfg2"]
+    x64 = ft.gen_inputs(1 << 20, torch.float64, 0, w.lo, w.hi, w.seed)
+    x32 = (x64 * 0.01).float()
+    eager = {"p64": ft.proposed_eval(x64, 7), "p32": ft.proposed_eval(x32, 7), "t32": ft.taylor_eval(x32, 5, 3)}
+    torch.cuda.synchronize()
+    outs = {"p64": {nm: torch.empty_like(x64) for nm in ("sin", "cos", "tan")},
+            "p32": {nm: torch.empty_like(x32) for nm in ("sin", "cos", "tan")},
+            "t32": {nm: torch.empty_like(x32) for nm in ("sin", "cos")}}
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        ft.proposed_eval(x64, 7, out=outs["p64"], stream=s)  # warm-up outside capture
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(3):
+                ft.proposed_eval(x64, 7, out=outs["p64"], stream=s)
+                ft.proposed_eval(x32, 7, out=outs["p32"], stream=s)
+                ft.taylor_eval(x32, 5, 3, out=outs["t32"], stream=s)
+    for o in outs.values():
+        for t in o.values():
+            t.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for k in eager:
+        for nm, t in eager[k].items():
+            assert torch.equal(t.view(torch.int64 if t.dtype == torch.float64 else torch.int32),
+                               outs[k][nm].view(torch.int64 if t.dtype == torch.float64 else torch.int32)), (k, nm)
