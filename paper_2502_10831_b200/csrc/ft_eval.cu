@@ -25,6 +25,15 @@ constexpr int kThreads = 256;
 #ifndef FT_TMA_TAYLOR_F32
 #define FT_TMA_TAYLOR_F32 0
 #endif
+// TMA-store kernels: threads per block and vectors per thread per tile.
+#ifndef FT_TMA_THREADS
+#define FT_TMA_THREADS 256
+#endif
+#ifndef FT_TMA_VPT
+#define FT_TMA_VPT 1
+#endif
+constexpr unsigned kTmaThreads = FT_TMA_THREADS;
+constexpr int kTmaVpt = FT_TMA_VPT;
 template <typename T>
 constexpr bool kTmaK1 = sizeof(T) == 8 && FT_TMA_F64;
 template <typename T>
@@ -33,7 +42,10 @@ constexpr bool kTmaK2 = (sizeof(T) == 8 && FT_TMA_F64) || (sizeof(T) == 4 && FT_
 #define FT_MINB_F32 4  // resident blocks/SM the f32 kernels are compiled for (register cap)
 #endif
 template <typename T>
-constexpr int kMinBlocks = kTmaK1<T> ? 3 : FT_MINB_F32;
+constexpr int kMinBlocks = kTmaK1<T> ? 3 * 256 / kTmaThreads : FT_MINB_F32;
+// Block size per kernel family (TMA-store kernels may differ, FT_TMA_THREADS).
+template <typename T>
+constexpr unsigned kBlockK1 = kTmaK1<T> ? kTmaThreads : kThreads;
 // K2 f32 (Taylor, 40 registers suffice): 6 resident blocks/SM measured +4.8%
 // over 4 (cfg4 f32: 4 -> 5 -> 6 blocks 434 -> 449 -> 454 Gelem/s; 8 spills);
 // K1 f32 loses 2-6% at 5.
@@ -44,7 +56,9 @@ constexpr int kMinBlocks = kTmaK1<T> ? 3 : FT_MINB_F32;
 // so those keep K1's 4 blocks/SM.
 template <typename T, unsigned MASK>
 constexpr int kMinBlocksK2 =
-    kTmaK2<T> ? 3 : (sizeof(T) == 4 && (MASK & kTan) == 0 ? FT_MINB_K2_F32 : FT_MINB_F32);
+    kTmaK2<T> ? 3 * 256 / kTmaThreads : (sizeof(T) == 4 && (MASK & kTan) == 0 ? FT_MINB_K2_F32 : FT_MINB_F32);
+template <typename T>
+constexpr unsigned kBlockK2 = kTmaK2<T> ? kTmaThreads : kThreads;
 // Where the exact-path branch sits: 0 one per element; 1 one per vector for
 // tan-only kernels (cfg3 +5%; the fused kernels lose 10% to the extra live
 // registers at the 64-register cap); 2 one per vector everywhere.
@@ -215,45 +229,57 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
       if constexpr ((MASK & kTan) != 0) st_out(reinterpret_cast<VT*>(o2) + v, res[2]);
     };
     if constexpr (TMA && !SEG) {
-      // Block tiles of kThreads vectors; x register-prefetched one tile ahead;
+      // Block tiles of kTmaVpt x kTmaThreads vectors (each thread kTmaVpt
+      // vectors, kTmaThreads apart); x register-prefetched one tile ahead;
       // outputs staged in a 3-slot shared-memory ring and written by one
       // thread as one TMA bulk store per output array per tile.  One barrier
       // per tile: after issuing tile i, thread 0 waits until the bulk store of
       // tile i-1 has read its slot; the next barrier publishes that to every
       // thread before the slot is refilled (tile i+2).
-      __shared__ __align__(128) VT stage[3][3][kThreads];
-      const unsigned nt = nv / kThreads;
+      constexpr unsigned kTile = kTmaVpt * kTmaThreads;
+      __shared__ __align__(128) VT stage[3][3][kTile];
+      const unsigned nt = nv / kTile;
       unsigned t = blockIdx.x;
-      VT cur{};
-      if (t < nt) cur = __ldcs(xv + (t * kThreads + threadIdx.x));
+      VT cur[kTmaVpt];
+#pragma unroll
+      for (int k = 0; k < kTmaVpt; ++k) cur[k] = VT{};
+      if (t < nt) {
+#pragma unroll
+        for (int k = 0; k < kTmaVpt; ++k) cur[k] = __ldcs(xv + (t * kTile + k * kTmaThreads + threadIdx.x));
+      }
       unsigned slot = 0;
       for (; t < nt; t += gridDim.x, slot = slot == 2 ? 0 : slot + 1) {
-        VT nxt{};
-#if FT_ADDR32
-        // 32-bit element index, one IMAD.WIDE.U32 for the address
-        if (t + gridDim.x < nt) nxt = __ldcs(xv + ((t + gridDim.x) * kThreads + threadIdx.x));
-#else
-        if (t + gridDim.x < nt) nxt = __ldcs(xv + (t + gridDim.x) * kThreads + threadIdx.x);
-#endif
-        VT res[3];
-        compute(cur, t * kThreads + threadIdx.x, res);
-        cur = nxt;
+        VT nxt[kTmaVpt];
 #pragma unroll
-        for (int j = 0; j < 3; ++j)
-          if (MASK & (1u << j)) stage[slot][j][threadIdx.x] = res[j];
+        for (int k = 0; k < kTmaVpt; ++k) nxt[k] = VT{};
+        if (t + gridDim.x < nt) {
+#pragma unroll
+          for (int k = 0; k < kTmaVpt; ++k)  // 32-bit element index: one IMAD.WIDE.U32 per address
+            nxt[k] = __ldcs(xv + ((t + gridDim.x) * kTile + k * kTmaThreads + threadIdx.x));
+        }
+#pragma unroll
+        for (int k = 0; k < kTmaVpt; ++k) {
+          VT res[3];
+          compute(cur[k], t * kTile + k * kTmaThreads + threadIdx.x, res);
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (MASK & (1u << j)) stage[slot][j][k * kTmaThreads + threadIdx.x] = res[j];
+        }
+#pragma unroll
+        for (int k = 0; k < kTmaVpt; ++k) cur[k] = nxt[k];
         fence_proxy_async_smem();
         __syncthreads();
         if (threadIdx.x == 0) {
 #pragma unroll
           for (int j = 0; j < 3; ++j)
             if (MASK & (1u << j))
-              bulk_store(reinterpret_cast<VT*>(j == 0 ? o0 : j == 1 ? o1 : o2) + t * kThreads,
-                         &stage[slot][j][0], kThreads * sizeof(VT));
+              bulk_store(reinterpret_cast<VT*>(j == 0 ? o0 : j == 1 ? o1 : o2) + t * kTile,
+                         &stage[slot][j][0], kTile * sizeof(VT));
           bulk_commit();
           bulk_wait_read_1();  // tile i-1's slot is free once the next barrier passes
         }
       }
-      for (unsigned v = nt * kThreads + tid; v < nv; v += stride) body(__ldcs(xv + v), v);
+      for (unsigned v = nt * kTile + tid; v < nv; v += stride) body(__ldcs(xv + v), v);
       if (threadIdx.x == 0) bulk_wait_all();
     } else {
 #if FT_RPF
@@ -480,7 +506,7 @@ struct MirrorOp {
 
 // ---------------- K1 ----------------
 template <typename T, int SQ, unsigned MASK, bool SEG>
-__global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_proposed(const EvalArgs a) {
+__global__ void __launch_bounds__(kBlockK1<T>, kMinBlocks<T>) k_proposed(const EvalArgs a) {
   __shared__ SmemTable tb;
   stage_table(&tb);
   pdl_wait();
@@ -490,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks<T>) k_proposed(const Eval
 
 // ---------------- K2 ----------------
 template <typename T, int NT, unsigned MASK>
-__global__ void __launch_bounds__(kThreads, (kMinBlocksK2<T, MASK>)) k_taylor(const EvalArgs a) {
+__global__ void __launch_bounds__(kBlockK2<T>, (kMinBlocksK2<T, MASK>)) k_taylor(const EvalArgs a) {
   using Op = TaylorOp<NT, MASK, sizeof(T) == 4>;  // certify-or-redo for the instruction-bound f32 kernels
   pdl_wait();
   stream_map<T, MASK, false, Op, kTmaK2<T>>(a, Op{a.steps});
@@ -555,13 +581,14 @@ bool pdl_enabled() {
 }
 
 template <class K>
-cudaError_t go(K kernel, const EvalArgs& a, cudaStream_t s, int waves = 0) {
+cudaError_t go(K kernel, const EvalArgs& a, cudaStream_t s, int waves = 0, unsigned threads = kThreads) {
   unsigned blocks = 0;
-  if (const cudaError_t eg = persistent_blocks(reinterpret_cast<const void*>(kernel), kThreads, a.n, &blocks, waves))
+  if (const cudaError_t eg = persistent_blocks(reinterpret_cast<const void*>(kernel), static_cast<int>(threads), a.n,
+                                               &blocks, waves))
     return eg;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -587,12 +614,12 @@ cudaError_t go(K kernel, const EvalArgs& a, cudaStream_t s, int waves = 0) {
 
 template <typename T, int SQ, bool SEG>
 cudaError_t proposed_t(unsigned mask, const EvalArgs& a, cudaStream_t s) {
-  FT_MASK_SWITCH(mask, (go(k_proposed<T, SQ, M, SEG>, a, s)))
+  FT_MASK_SWITCH(mask, (go(k_proposed<T, SQ, M, SEG>, a, s, 0, kBlockK1<T>)))
 }
 
 template <typename T, int NT>
 cudaError_t taylor_t(unsigned mask, const EvalArgs& a, cudaStream_t s) {
-  FT_MASK_SWITCH(mask, (go(k_taylor<T, NT, M>, a, s)))
+  FT_MASK_SWITCH(mask, (go(k_taylor<T, NT, M>, a, s, 0, kBlockK2<T>)))
 }
 
 template <int SQ, bool SEG>
