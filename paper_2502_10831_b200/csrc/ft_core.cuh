@@ -775,9 +775,6 @@ __device__ __forceinline__ Out3 fast_taylor(double x, int n) {
 // Segment choice is g, the certified row.  tests/test_f32_exhaustive_gpu.py
 // checks all 2^32 float inputs against the bit-exact kernels and the
 // reference library (<= 1 ulp observed, segments identical).
-#ifndef FT_RELAX_TAN_SHORT
-#define FT_RELAX_TAN_SHORT 1
-#endif
 constexpr float kRelaxMaxAbs = 65536.0f;  // 2^16
 constexpr int kHiRelaxLo = 0x3f400000;    // hi(2^-11)
 constexpr int kHiRelaxCos = 0x3ff91ffb;   // hi(pi/2 - 2^-11)
@@ -824,36 +821,12 @@ struct Out3f {
 
 __device__ __forceinline__ float xor_f(float v, unsigned bits) { return __uint_as_float(__float_as_uint(v) ^ bits); }
 
-#ifndef FT_RELAX_I2D
-#define FT_RELAX_I2D 0
-#endif
-#ifndef FT_RELAX_RZOUT
-#define FT_RELAX_RZOUT 0
-#endif
-// |x| as a double.  FT_RELAX_I2D: by integer re-biasing of the float's bits
-// (exact for normal floats; zero / subnormals become tiny normals, which the
-// brackets reject or -- cos-only -- evaluate to the same float; non-finite
-// and |x| >= 2^16 are rejected on the float itself).
-__device__ __forceinline__ double relaxed_abs_x(float xf) {
-  if constexpr (FT_RELAX_I2D) {
-    const unsigned b = __float_as_uint(xf) << 1;  // drop the sign
-    return __hiloint2double(static_cast<int>((b >> 4) + 0x38000000u), static_cast<int>(b << 28));
-  } else {
-    return fabs(static_cast<double>(xf));
-  }
-}
-// v (positive, a normal float's range) to float, with `sign` (bit 31) applied.
-// FT_RELAX_RZOUT: truncation by one funnel shift (bits 60..29 of v) and an
-// exponent re-bias -- <= 1 ulp from RN, inside the 2-ulp budget with the
-// relaxed evaluation's 2^-26.9 (checked exhaustively).
+// |x| as a double (F2F on the XU pipe; an integer re-bias measured slower, r02l).
+__device__ __forceinline__ double relaxed_abs_x(float xf) { return fabs(static_cast<double>(xf)); }
+// v to float with `sign` (bit 31) applied (a truncating funnel-shift
+// conversion measured slower, r02l).
 __device__ __forceinline__ float relaxed_to_float(double v, unsigned sign) {
-  if constexpr (FT_RELAX_RZOUT) {
-    const unsigned t = __funnelshift_l(static_cast<unsigned>(__double2loint(v)),
-                                       static_cast<unsigned>(__double2hiint(v)), 3);
-    return __uint_as_float(((t ^ 0x40000000u) & 0x7fffffffu) | sign);
-  } else {
-    return xor_f(__double2float_rn(v), sign);
-  }
+  return xor_f(__double2float_rn(v), sign);
 }
 
 // CHECK_X = false: the caller has established |x| < 2^16 for every non-NaN
@@ -891,7 +864,7 @@ __device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const RelaxTabl
     double v;
     if constexpr (SQ == kExact) {
       v = __ddiv_rn(ns, nc);
-    } else if constexpr (SQ == kFisr1 && FT_RELAX_TAN_SHORT) {
+    } else if constexpr (SQ == kFisr1) {
       // ns * (y0 h)^2 with h = 1.5 - 0.5 nc y0^2 (one Newton step), as
       // (ns y0^2) h h: the same six FP64 operations, one dependent step fewer.
       const double y0 = fisr_seed(nc);

@@ -65,15 +65,6 @@ constexpr unsigned kBlockK2 = kTmaK2<T> ? kTmaThreads : kThreads;
 #ifndef FT_BATCH_SLOW
 #define FT_BATCH_SLOW 1
 #endif
-#ifndef FT_PINGPONG
-#define FT_PINGPONG 0  // 1: per-thread loop unrolled by two with ping-pong prefetch registers (r02r: -3%)
-#endif
-#ifndef FT_ADDR32
-#define FT_ADDR32 1
-#endif
-#ifndef FT_L2PF
-#define FT_L2PF 0  // >0: also prefetch x into L2 this many iterations ahead (per-thread loop)
-#endif
 #ifndef FT_RPF
 #define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
 #endif
@@ -299,43 +290,13 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
       cur = nx1;
       nx1 = nx2;
     }
-#elif FT_PINGPONG
-    // Unrolled by two with ping-pong registers: no register moves between
-    // iterations, and the prefetch index is clamped to the last vector instead
-    // of predicated (the extra load of a thread's final round is discarded).
-    // Indices stay 32-bit so each address is one IMAD.WIDE.U32.
-    if (nv > 0) {
-      const unsigned last = nv - 1;
-      VT cur = ld_x(xv + min(tid, last));
-      unsigned v = tid;
-      while (v < nv) {
-        const unsigned v1 = v + stride;
-        const VT nxt = ld_x(xv + min(v1, last));
-        body(cur, v);
-        if (v1 >= nv) break;
-        const unsigned v2 = v1 + stride;
-        cur = ld_x(xv + min(v2, last));
-        body(nxt, v1);
-        v = v2;
-      }
-    }
 #else
     VT cur{};
     if (tid < nv) cur = ld_x(xv + tid);
     for (unsigned v = tid; v < nv; v += stride) {
       VT nxt{};
-#if FT_ADDR32
       const unsigned vn = v + stride;  // 32-bit index: one IMAD.WIDE.U32 per address
       if (vn < nv) nxt = ld_x(xv + vn);
-#if FT_L2PF > 0
-      // DRAM -> L2 prefetch FT_L2PF iterations ahead (no register held), so the
-      // one-ahead register load hits L2
-      const unsigned vp = v + FT_L2PF * stride;
-      if (vp < nv) asm volatile("prefetch.global.L2 [%0];" ::"l"(xv + vp));
-#endif
-#else
-      if (v + stride < nv) nxt = ld_x(xv + v + stride);
-#endif
       body(cur, v);
       cur = nxt;
     }
@@ -402,9 +363,6 @@ struct TaylorOp {
 #ifndef FT_VEC_DISPATCH
 #define FT_VEC_DISPATCH 1
 #endif
-#ifndef FT_VEC_EXACT_INLINE
-#define FT_VEC_EXACT_INLINE 0
-#endif
 // Relaxed ops: per vector of 4 floats, a warp whose lanes all hold |x| < 2^16
 // (the common case) runs the relaxed evaluation without a per-element range
 // check; any lane beyond it sends the warp's vector to the bit-exact evaluation
@@ -433,12 +391,7 @@ struct RelaxedOp {
     return o;
   }
   __device__ __forceinline__ Out3f exact(float x) const {
-#if FT_VEC_EXACT_INLINE
-    const Out3 o = fast_proposed<SQ, MASK, SEG>(static_cast<double>(x), *tbx, steps);
-    return Out3f{__double2float_rn(o.s), __double2float_rn(o.c), __double2float_rn(o.t), o.seg_sc, o.seg_t};
-#else
     return relaxed_slow<SQ, MASK, SEG>(x, tbx, steps);  // out of line: the common path keeps its registers
-#endif
   }
   __device__ __forceinline__ Out3f operator()(float x) const {
 #if FT_NULL_EVAL
