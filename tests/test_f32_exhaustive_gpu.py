@@ -200,3 +200,38 @@ def test_relaxed_golden_vectors_and_segments(ft, golden):
         assert np.array_equal(out["seg_t"].cpu().numpy(), ref["seg_t"]), (case, mode)
         n += x.size
     assert n > 5000
+
+
+@pytest.mark.parametrize("mask", [7, 4, 3])
+def test_relaxed_range_dispatch_mixed_warps(ft, mask):
+    """Warps holding any |x| >= 2^16 evaluate their vector bit-exactly (the
+    range dispatch of the relaxed kernels): dense and sparse large arguments,
+    NaN and infinities mixed into small ones -- within 2 ulp of the oracle and,
+    for the all-large vectors, bitwise equal to the bit-exact policy; Taylor too."""
+    rng = np.random.default_rng(7 + mask)
+    n = 1 << 20
+    small = rng.uniform(-300.0, 300.0, n).astype(np.float32)
+    cases = {}
+    x = small.copy()
+    x[::4] = rng.uniform(-1e7, 1e7, n // 4).astype(np.float32)  # every vector has a large lane
+    cases["dense"] = x
+    x = small.copy()
+    idx = rng.choice(n, n // 997, replace=False)
+    x[idx] = rng.uniform(-1e6, 1e6, idx.size).astype(np.float32)
+    x[idx[:50]] = np.array([np.inf, -np.inf, np.nan, 65536.0, -65535.99] * 10, np.float32)
+    cases["sparse"] = x
+    for name, x in cases.items():
+        xd = torch.from_numpy(x).cuda()
+        got = ft.proposed_eval(xd, mask)
+        with ft.f32_policy("bitwise"):
+            bit = ft.proposed_eval(xd, mask)
+        ref = O.proposed(x, mask)
+        for f in got:
+            g = got[f].cpu().numpy()
+            assert _ulp32(g, ref[f]) <= 2, (name, f)
+            if name == "dense":
+                assert np.array_equal(g.view(np.uint32), bit[f].cpu().numpy().view(np.uint32)), f
+        t = ft.taylor_eval(xd, 5, 3)
+        tr = O.taylor(x, 5, 3)
+        for f in t:
+            assert _ulp32(t[f].cpu().numpy(), tr[f]) <= 2, (name, "taylor", f)
