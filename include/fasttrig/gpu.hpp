@@ -66,6 +66,10 @@ constexpr ft_dtype dtype_of() {
 // device and host thread each; results do not depend on the setting.
 inline void set_devices(int n) { check(ft_set_host_devices(n)); }
 
+// Free the host-pointer pipeline and staging buffers of `device` (-1: all);
+// they are re-created on demand.
+inline void release(int device = -1) { check(ft_release(device)); }
+
 // ---- reference-shaped batch calls (host memory in, host memory out) ----
 inline std::vector<double> proposed_sin_batch(std::span<const double> xs, SqrtMode mode = {}) {
   std::vector<double> out(xs.size());

@@ -89,6 +89,11 @@ int main() {
   }
   EXPECT(threw);
 
+  // release the pipeline buffers; the next call re-creates them
+  g::release();
+  auto again = g::proposed_sin_batch(xs);
+  EXPECT(std::memcmp(again.data(), s.data(), xs.size() * 8) == 0);
+
   std::printf("gpu.hpp drop-in: %s (%d failures)\n", failures ? "FAIL" : "OK", failures);
   return failures ? 1 : 0;
 }
