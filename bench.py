@@ -576,6 +576,25 @@ def e2e_pageable(ctx: Ctx, w, state, steps: int, n_e2e: int) -> dict:
         _lib.check(L.ft_proposed_batch_host(_lib.FT_F64, x.ctypes.data, n_e2e, 7, mode,
                                             *[outs[nm].ctypes.data for nm in ("sin", "cos", "tan")]))
 
+    # the C++ drop-in itself (gpu.hpp: std::vector in, a new std::vector out per call)
+    exe = os.path.join(ROOT, "paper_2502_10831_b200", "lib", "bench_dropin")
+    if ctx.world == 1 and os.path.exists(exe):
+        try:
+            r = subprocess.run([exe, str(n_e2e), str(steps)], capture_output=True, text=True, timeout=600)
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            for key, val, note in (
+                    ("cpp_gpu_hpp_x3_std_vector", d["api_x3_std_vector_gelem_s"],
+                     "three calls, each returning a new std::vector"),
+                    ("cpp_gpu_hpp_fused_std_vector", d["fused_std_vector_gelem_s"],
+                     "proposed_sincostan_batch returning three new std::vectors"),
+                    ("cpp_gpu_hpp_span_out", d["span_out_preallocated_gelem_s"],
+                     "proposed_batch into caller-owned (pageable) vectors")):
+                res[key] = {"value": round(val, 6), "unit": "Gelem/s", "elements_per_step_per_gpu": n_e2e,
+                            "steps": steps, "call": note,
+                            "new_std_vector_seconds": d["new_std_vector_seconds"],
+                            "timing": "host steady_clock around the C++ calls (tools/bench_dropin.cpp)"}
+        except Exception as e:  # noqa: BLE001 -- report, do not fail the bench line
+            res["cpp_gpu_hpp_std_vector"] = {"error": repr(e)[:200]}
     for name, fn, h2d in (("api_single_output_x3_pageable", three, 3), ("fused_pageable", fused, 1)):
         fn()  # warm
         ctx.barrier()

@@ -66,7 +66,8 @@ def test_our_arm_line():
     su = d["sustained"]
     assert su["value"] > 0 and su["seconds"] >= 1.5 and "sm_mhz" in su["clocks"]
     ev = d["e2e_variants"]
-    assert set(ev) == {"api_single_output_x3_pageable", "fused_pageable"}
+    assert set(ev) == {"api_single_output_x3_pageable", "fused_pageable", "cpp_gpu_hpp_x3_std_vector",
+                       "cpp_gpu_hpp_fused_std_vector", "cpp_gpu_hpp_span_out"}
     assert all(v["value"] > 0 for v in ev.values())
     assert set(d["configs"]) == {"cfg1", "cfg3", "cfg4_f32"}
     for name, c in d["configs"].items():
