@@ -829,9 +829,7 @@ __device__ __forceinline__ float relaxed_to_float(double v, unsigned sign) {
   return xor_f(__double2float_rn(v), sign);
 }
 
-// CHECK_X = false: the caller has established |x| < 2^16 for every non-NaN
-// lane (vector-level dispatch in stream_map); NaN still fails the bracket.
-template <int SQ, unsigned MASK, bool SEG, bool CHECK_X = true>
+template <int SQ, unsigned MASK, bool SEG>
 __device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const RelaxTable& tb, int steps, bool* okp) {
   constexpr bool kS = (MASK & kSin) != 0, kC = (MASK & kCos) != 0, kT = (MASK & kTan) != 0;
   const FastConsts& K = c_fast;
@@ -843,8 +841,7 @@ __device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const RelaxTabl
   const unsigned ra = static_cast<unsigned>(__cvta_generic_to_shared(&tb)) + g * sizeof(RelaxRow);
   const int2 br = lds_i32x2(ra + offsetof(RelaxRow, klo_hi));
   const int h = __double2hiint(d) & 0x7fffffff;
-  bool ok = (h > br.x) & (h < br.y);
-  if constexpr (CHECK_X) ok = ok & (fabsf(xf) < kRelaxMaxAbs);
+  bool ok = (fabsf(xf) < kRelaxMaxAbs) & (h > br.x) & (h < br.y);
   if constexpr (kT || SEG) ok = ok & (h != kHiGuard);
   const unsigned modd = static_cast<unsigned>(__double2loint(t)) << 31;  // m odd
   const unsigned dx = static_cast<unsigned>(__double2hiint(d)) ^ __float_as_uint(xf);
@@ -898,7 +895,7 @@ static __device__ __noinline__ Out3f relaxed_slow(float xf, const SmemTable* tbx
 // Horner contracted to FMAs.  Brackets: red >= 2^-11 for sin and tan (zero at
 // 0), red <= pi/2 - 2^-11 for cos (the truncated cosine's zero lies within
 // 2.5e-5 of pi/2 for these NT: Taylor-5 cos(pi/2) = -2.47e-5).
-template <int NT, unsigned MASK, bool CHECK_X = true>
+template <int NT, unsigned MASK>
 __device__ __forceinline__ Out3f relaxed_taylor_core(float xf, bool* okp) {
   constexpr bool kS = (MASK & kSin) != 0, kC = (MASK & kCos) != 0, kT = (MASK & kTan) != 0;
   const FastConsts& K = c_fast;
@@ -907,8 +904,7 @@ __device__ __forceinline__ Out3f relaxed_taylor_core(float xf, bool* okp) {
   const double d = __fma_rn(-K.pi, __dadd_rn(t, -kRintMagic), a);
   const double red = fabs(d);
   const int h = __double2hiint(d) & 0x7fffffff;
-  bool ok = !CHECK_X || fabsf(xf) < kRelaxMaxAbs;
-  if constexpr (!CHECK_X) ok = ok & (h < 0x7ff00000);  // NaN x (not caught by the vector check)
+  bool ok = fabsf(xf) < kRelaxMaxAbs;
   if constexpr (kS || kT) ok = ok & (h > kHiRelaxLo);
   ok = ok & (h < (kC ? kHiRelaxCos : kHiHalfPi));
   const unsigned modd = static_cast<unsigned>(__double2loint(t)) << 31;

@@ -164,15 +164,7 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
         g1[j] = static_cast<std::uint8_t>(o.seg_t);
       };
       constexpr int G = Op::template kGroup<T> < VN ? Op::template kGroup<T> : VN;
-      if constexpr (Op::kVecDispatch) {
-        if (op.vec_exact(xs)) {
-#pragma unroll
-          for (int j = 0; j < VN; ++j) put(j, op.exact(xs[j]));
-        } else {
-#pragma unroll
-          for (int j = 0; j < VN; ++j) put(j, op.vec(xs[j]));
-        }
-      } else if constexpr (G > 1) {
+      if constexpr (G > 1) {
         // Groups of G elements: the fast path of every element of the group
         // first (no branch between them, so the compiler can interleave their
         // dependency chains), then one rarely-taken branch that redoes the
@@ -324,7 +316,6 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
 
 template <int SQ, unsigned MASK, bool SEG>
 struct ProposedOp {
-  static constexpr bool kVecDispatch = false;
   // Elements per exact-path branch (see stream_map).
   template <typename T>
   static constexpr int kGroup =
@@ -342,7 +333,6 @@ struct ProposedOp {
 
 template <int NT, unsigned MASK, bool CERT>
 struct TaylorOp {
-  static constexpr bool kVecDispatch = false;
   template <typename T>
   static constexpr int kGroup = 1;
   int n;
@@ -360,39 +350,13 @@ struct TaylorOp {
 #ifndef FT_RELAX_GROUP_TAN
 #define FT_RELAX_GROUP_TAN 1  // the same for the tan-only relaxed kernels
 #endif
-#ifndef FT_VEC_DISPATCH
-#define FT_VEC_DISPATCH 1
-#endif
-// Relaxed ops: per vector of 4 floats, a warp whose lanes all hold |x| < 2^16
-// (the common case) runs the relaxed evaluation without a per-element range
-// check; any lane beyond it sends the warp's vector to the bit-exact evaluation
-// directly, out of line (no wasted relaxed attempt).  f32 inputs with |x| >=
-// 2^16 ran at half the bit-exact kernel's rate without this (150 vs 300
-// Gelem/s) and at ~70% of it with it (210), for ~1% on the |x| < 2^16 configs
-// (tools/policy_probe.py, profiles/r02_variants.jsonl r02ad-ag).
-__device__ __forceinline__ bool warp_any_big(const float* xs) {
-  const float m = fmaxf(fmaxf(fabsf(xs[0]), fabsf(xs[1])), fmaxf(fabsf(xs[2]), fabsf(xs[3])));
-  return __any_sync(__activemask(), !(m < kRelaxMaxAbs));  // NaN lanes pass; the bracket rejects them
-}
-
 template <int SQ, unsigned MASK, bool SEG>
 struct RelaxedOp {
   template <typename T>
   static constexpr int kGroup = MASK == kTan ? FT_RELAX_GROUP_TAN : FT_RELAX_GROUP;
-  static constexpr bool kVecDispatch = FT_VEC_DISPATCH && !FT_NULL_EVAL && kGroup<float> == 1;
   const RelaxTable* tb;  // relaxed rows
   const SmemTable* tbx;  // bit-exact rows (fallback)
   int steps;
-  __device__ __forceinline__ bool vec_exact(const float* xs) const { return warp_any_big(xs); }
-  __device__ __forceinline__ Out3f vec(float x) const {  // |x| < 2^16 or NaN
-    bool ok;
-    Out3f o = relaxed_proposed_core<SQ, MASK, SEG, false>(x, *tb, steps, &ok);
-    if (!ok) o = relaxed_slow<SQ, MASK, SEG>(x, tbx, steps);  // rare
-    return o;
-  }
-  __device__ __forceinline__ Out3f exact(float x) const {
-    return relaxed_slow<SQ, MASK, SEG>(x, tbx, steps);  // out of line: the common path keeps its registers
-  }
   __device__ __forceinline__ Out3f operator()(float x) const {
 #if FT_NULL_EVAL
     return Out3f{x, x, x, 0, 0};  // measurement-only build: the kernel's traffic without its math
@@ -412,15 +376,6 @@ template <int NT, unsigned MASK>
 struct RelaxedTaylorOp {
   template <typename T>
   static constexpr int kGroup = FT_RELAX_GROUP;
-  static constexpr bool kVecDispatch = FT_VEC_DISPATCH && FT_RELAX_GROUP == 1;
-  __device__ __forceinline__ bool vec_exact(const float* xs) const { return warp_any_big(xs); }
-  __device__ __forceinline__ Out3f vec(float x) const {
-    bool ok;
-    Out3f o = relaxed_taylor_core<NT, MASK, false>(x, &ok);
-    if (!ok) o = relaxed_taylor_slow<NT, MASK>(x);  // rare
-    return o;
-  }
-  __device__ __forceinline__ Out3f exact(float x) const { return relaxed_taylor_slow<NT, MASK>(x); }
   __device__ __forceinline__ Out3f operator()(float x) const {
     bool ok;
     Out3f o = relaxed_taylor_core<NT, MASK>(x, &ok);
@@ -435,7 +390,6 @@ struct RelaxedTaylorOp {
 // reference scalar code does (kernels.hpp:46-67 / SPEC.md:224-247).
 template <unsigned MASK>
 struct MirrorOp {
-  static constexpr bool kVecDispatch = false;
   template <typename T>
   static constexpr int kGroup = 1;
   int kind, method, steps, n;

@@ -226,11 +226,21 @@ def test_relaxed_range_dispatch_mixed_warps(ft, mask):
         with ft.f32_policy("bitwise"):
             bit = ft.proposed_eval(xd, mask)
         ref = O.proposed(x, mask)
+        big = ~(np.abs(x) < 65536.0)
+        one = {f: np.concatenate([ft.proposed_eval(xd[i:i + 1], mask)[f].cpu().numpy()
+                                  for i in range(0, 64)]) for f in got}  # scalar path, one element each
         for f in got:
             g = got[f].cpu().numpy()
             assert _ulp32(g, ref[f]) <= 2, (name, f)
-            if name == "dense":
-                assert np.array_equal(g.view(np.uint32), bit[f].cpu().numpy().view(np.uint32)), f
+            # large arguments are bit-exact; every element is what the scalar path gives it
+            assert np.array_equal(g[big].view(np.uint32), bit[f].cpu().numpy()[big].view(np.uint32)), f
+            assert np.array_equal(g[:64].view(np.uint32), one[f].view(np.uint32)), (name, f)
+        # the unaligned view runs the scalar path on every element: same bits
+        buf = torch.empty(n + 1, dtype=torch.float32, device="cuda")
+        buf[1:].copy_(xd)
+        shifted = ft.proposed_eval(buf[1:], mask)
+        for f in got:
+            assert torch.equal(shifted[f].view(torch.int32), got[f].view(torch.int32)), (name, f)
         t = ft.taylor_eval(xd, 5, 3)
         tr = O.taylor(x, 5, 3)
         for f in t:
