@@ -65,6 +65,9 @@ constexpr unsigned kBlockK2 = kTmaK2<T> ? kTmaThreads : kThreads;
 #ifndef FT_BATCH_SLOW
 #define FT_BATCH_SLOW 1
 #endif
+#ifndef FT_GROUP_RECHECK
+#define FT_GROUP_RECHECK 1  // relaxed kernels: the rare exact-path block re-derives which elements of the group failed
+#endif
 #ifndef FT_RPF
 #define FT_RPF 1  // 1: register prefetch of the next x (0: load at use)
 #endif
@@ -181,9 +184,25 @@ __device__ __forceinline__ void stream_map(const EvalArgs& a, const Op& op) {
             all = all && okv[j];
           }
           if (!all) {
+            if constexpr (Op::kRecheck) {
+              // Rare block: find the failing elements again from x itself (the
+              // opaque copy stops the compiler from keeping G pass/fail
+              // predicates alive across the branch, which it does by packing
+              // them into a register with ~5 extra instructions per element).
 #pragma unroll
-            for (int j = 0; j < G; ++j)
-              if (!okv[j]) ov[j] = op.slow(xs[j0 + j]);
+              for (int j = 0; j < G; ++j) {
+                T xj = xs[j0 + j];
+                if constexpr (sizeof(T) == 4) asm volatile("" : "+f"(xj));
+                else asm volatile("" : "+d"(xj));
+                bool okj;
+                (void)op.core(xj, &okj);
+                if (!okj) ov[j] = op.slow(xj);
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < G; ++j)
+                if (!okv[j]) ov[j] = op.slow(xs[j0 + j]);
+            }
           }
 #pragma unroll
           for (int j = 0; j < G; ++j) put(j0 + j, ov[j]);
@@ -320,6 +339,7 @@ struct ProposedOp {
   template <typename T>
   static constexpr int kGroup =
       FT_BATCH_SLOW == 2 ? 4 : (FT_BATCH_SLOW == 1 && MASK == kTan) ? 4 : 1;
+  static constexpr bool kRecheck = false;
   const SmemTable* tb;
   int steps;
   __device__ __forceinline__ Out3 operator()(double x) const {
@@ -335,6 +355,7 @@ template <int NT, unsigned MASK, bool CERT>
 struct TaylorOp {
   template <typename T>
   static constexpr int kGroup = 1;
+  static constexpr bool kRecheck = false;
   int n;
   __device__ __forceinline__ Out3 operator()(double x) const { return fast_taylor<NT, MASK, CERT>(x, n); }
 };
@@ -348,12 +369,13 @@ struct TaylorOp {
 #define FT_RELAX_GROUP 1  // elements per exact-path branch in the relaxed kernels
 #endif
 #ifndef FT_RELAX_GROUP_TAN
-#define FT_RELAX_GROUP_TAN 1  // the same for the tan-only relaxed kernels
+#define FT_RELAX_GROUP_TAN 2  // the same for the tan-only relaxed kernels (cfg3 +1.2% over 1, r02bb/bc; 4: -1.5%)
 #endif
 template <int SQ, unsigned MASK, bool SEG>
 struct RelaxedOp {
   template <typename T>
   static constexpr int kGroup = MASK == kTan ? FT_RELAX_GROUP_TAN : FT_RELAX_GROUP;
+  static constexpr bool kRecheck = FT_GROUP_RECHECK != 0;
   const RelaxTable* tb;  // relaxed rows
   const SmemTable* tbx;  // bit-exact rows (fallback)
   int steps;
@@ -376,6 +398,7 @@ template <int NT, unsigned MASK>
 struct RelaxedTaylorOp {
   template <typename T>
   static constexpr int kGroup = FT_RELAX_GROUP;
+  static constexpr bool kRecheck = FT_GROUP_RECHECK != 0;
   __device__ __forceinline__ Out3f operator()(float x) const {
     bool ok;
     Out3f o = relaxed_taylor_core<NT, MASK>(x, &ok);
@@ -392,6 +415,7 @@ template <unsigned MASK>
 struct MirrorOp {
   template <typename T>
   static constexpr int kGroup = 1;
+  static constexpr bool kRecheck = false;
   int kind, method, steps, n;
   __device__ __forceinline__ Out3 operator()(double x) const {
     Out3 o{0.0, 0.0, 0.0, 0, 0};
