@@ -28,7 +28,11 @@ events on the launching stream, barrier + synchronize on both sides, max over
 ranks.
 
 `sustained` repeats the headline step for ~20 s of device time (the
-power-capped steady state; the headline window is under a second).
+power-capped steady state; the headline window is under a second).  `burst`
+(headline and every config) is the best of 3 windows of ~20 ms of back-to-back
+steps, each after 1 s of idle and ~5 ms of untimed launches: the rate before
+the board-power limiter engages (~50 ms into a run, tools/power_ramp.py), i.e.
+the regime the HBM peak itself (best of 10 single copies) is measured in.
 
 `e2e` is the headline metric through the public host-pointer C-ABI call
 (ft_proposed_batch_host) with pinned host buffers over the full shard: every
@@ -397,7 +401,30 @@ def time_steps(step, k: int, stream) -> float:
     return e0.elapsed_time(e1) / k
 
 
-def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0, keep: bool = False):
+def burst_window(ctx: Ctx, step, stream, ms_hint: float, window_ms: float = 20.0, idle_s: float = 1.0,
+                 reps: int = 3) -> dict:
+    """Best of `reps` short windows (~`window_ms` of back-to-back steps, >= 3),
+    each after `idle_s` of idle and ~5 ms of untimed launches: the rate before
+    the board-power limiter engages (it does ~50 ms into a run of the f32
+    kernels, tools/power_ramp.py) -- the regime MEASURED_PEAKS.json's hbm_gbs
+    (best of 10 single copies) is measured in."""
+    import torch
+
+    k = max(3, int(window_ms / max(ms_hint, 1e-3)))
+    kw = max(3, int(5.0 / max(ms_hint, 1e-3)))
+    best = float("inf")
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        time.sleep(idle_s)
+        ctx.barrier()
+        for i in range(kw):
+            step(i)
+        best = min(best, ctx.max_over_ranks(time_steps(step, k, stream)))
+    return {"ms_per_step": best, "steps": k, "warmup": kw, "idle_s": idle_s, "reps": reps}
+
+
+def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0, keep: bool = False,
+            burst: bool = True):
     """Generate w's shard in place, time `steps` launches of its kernel, check
     the outputs with K3, all-reduce the statistics.  Returns (entry, state)."""
     import torch
@@ -437,6 +464,7 @@ def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0
         ctx.barrier()
         launches = ft.launch_count() - l0
         clk = clocks.stop()
+        bw = burst_window(ctx, step, stream, ms_local) if burst else None
     ms = ctx.max_over_ranks(ms_local)
     value = total / (ms / 1e3) / 1e9
 
@@ -463,12 +491,17 @@ def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0
         "nan_count": st["n_nan"], "checksum": st["checksum"], "outputs": names,
         "oracle": "device restatement of the reference (ft_mirror_*), bitwise-pinned to the CPU oracle",
     }
+    if bw:
+        bms = bw["ms_per_step"]
+        bw = {"value": round(total / (bms / 1e3) / 1e9, 4), "unit": "Gelem/s", "ms_per_step": round(bms, 5),
+              "steps": bw["steps"], "warmup": bw["warmup"], "idle_s": bw["idle_s"], "best_of": bw["reps"],
+              "roofline_frac": round(w.bytes_per_elem * n / (bms / 1e3) / 1e9 / peak, 4)}
     entry = {"value": round(value, 4), "unit": "Gelem/s", "per_gpu_gelem_s": round(n / (ms / 1e3) / 1e9, 4),
              "ms_per_step": round(ms, 5), "steps": steps, "warmup": max(warmup, 3), "scaling": scaling,
              "dtype": "f64" if w.itemsize == 8 else "f32",
              "config": config_dict(w, n, ctx.world, policy, rot), "roofline": roofline,
              "fp64_roof": fp64_roof(w.name, n / (ms_local / 1e3) / 1e9), "gpu_launches": int(launches),
-             "clocks": clk, "accuracy": accuracy}
+             "clocks": clk, "burst": bw, "accuracy": accuracy}
     state = {"x": x, "out": out, "n": n, "total": total, "names": names, "tdt": tdt} if keep else None
     del sets
     if not keep:
@@ -620,7 +653,8 @@ def run_ours(args) -> None:
     ctx = Ctx(args)
     _lib.lib()  # fail loudly if the CUDA library is missing
     w = CONFIGS[args.config]
-    head, state = measure(ctx, w, args.steps, args.warmup, args.f32_policy, args.elements, keep=True)
+    head, state = measure(ctx, w, args.steps, args.warmup, args.f32_policy, args.elements, keep=True,
+                          burst=not args.no_burst)
 
     sus = None
     if args.sustained_seconds > 0:
@@ -660,7 +694,7 @@ def run_ours(args) -> None:
              else [] if sel == "auto" else [c for c in sel.split(",") if c and c != w.name])
     for c in names:
         k = args.config_steps or CONFIG_STEPS.get(c, 100)
-        e, _ = measure(ctx, CONFIGS[c], k, min(args.warmup, 10), args.f32_policy)
+        e, _ = measure(ctx, CONFIGS[c], k, min(args.warmup, 10), args.f32_policy, burst=not args.no_burst)
         extra[c] = e
 
     if ctx.rank == 0:
@@ -671,7 +705,8 @@ def run_ours(args) -> None:
             "dtype": head["dtype"], "data": "synthetic", "config": head["config"],
             "per_gpu_gelem_s": head["per_gpu_gelem_s"], "roofline": head["roofline"],
             "fp64_roof": head["fp64_roof"], "cpu_baseline": cpu, "e2e": e2e, "e2e_variants": e2e_var,
-            "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "sustained": sus,
+            "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "burst": head["burst"],
+            "sustained": sus,
             "accuracy": head["accuracy"],
             "configs": extra or None,
         }
@@ -704,6 +739,7 @@ def main() -> None:
     ap.add_argument("--e2e-elements", type=int, default=0,
                     help="elements per rank per e2e step (default: the whole shard)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-burst", action="store_true", help="skip the short-window (pre-power-cap) timing")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

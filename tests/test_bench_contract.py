@@ -63,6 +63,9 @@ def test_our_arm_line():
     assert d["accuracy"]["max_ulp_vs_oracle"] == [0, 0, 0]
     assert d["accuracy"]["bit_mismatch_vs_oracle"] == [0, 0, 0]
     assert d["cpu_baseline"]["value"] > 0
+    bu = d["burst"]
+    assert bu["value"] > 0 and bu["steps"] >= 3 and 0 < bu["roofline_frac"] < 1.2
+    assert all(c["burst"]["value"] > 0 for c in d["configs"].values())
     su = d["sustained"]
     assert su["value"] > 0 and su["seconds"] >= 1.5 and "sm_mhz" in su["clocks"]
     ev = d["e2e_variants"]
