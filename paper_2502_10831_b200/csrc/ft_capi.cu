@@ -554,6 +554,12 @@ cudaError_t persistent_blocks(const void* fn, int threads, std::size_t work_item
     const int m = env ? std::atoi(env) : 4;
     return m >= 1 ? m : 1;
   }();
+  // FT_OCC_CAP (experiments): size the grid for at most this many blocks per SM.
+  static const int occ_cap = [] {
+    const char* env = std::getenv("FT_OCC_CAP");
+    return env ? std::atoi(env) : 0;
+  }();
+  if (occ_cap >= 1 && occ > occ_cap) occ = occ_cap;
   const std::size_t need = (work_items + threads - 1) / threads;
   const std::size_t full = static_cast<std::size_t>(occ) * sms * (waves > 0 ? waves : mult);
   *blocks = static_cast<unsigned>(std::max<std::size_t>(1, std::min(need, full)));
