@@ -875,9 +875,11 @@ __device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const RelaxTabl
   const double ns = __fma_rn(ca, red, cb);  // sine numerator == tangent numerator
   const double nc = __fma_rn(cc, red, cd);  // cosine numerator == tangent denominator
   Out3f o{0.0f, 0.0f, 0.0f, 0, 0};
+  const unsigned sd = dx & 0x80000000u;  // sign of the folded angle: sin, tan and the guard's infinity
   if constexpr (kS || kC) {
-    const double rs = fast_rsqrt<SQ>(__fma_rn(ns, ns, __dmul_rn(nc, nc)), steps);
-    if constexpr (kS) o.s = relaxed_to_float(__dmul_rn(ns, rs), (dx ^ modd) & 0x80000000u);
+    const double rad = __fma_rn(ns, ns, __dmul_rn(nc, nc));
+    const double rs = fast_rsqrt<SQ>(rad, steps);
+    if constexpr (kS) o.s = xor_f(xor_f(__double2float_rn(__dmul_rn(ns, rs)), modd), sd);  // one 3-input LOP3
     if constexpr (kC) o.c = relaxed_to_float(__dmul_rn(nc, rs), modd);
   }
   const bool guard = h > kHiGuard;
@@ -896,8 +898,8 @@ __device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const RelaxTabl
       const double r = fast_rsqrt<SQ>(nc, steps);
       v = __dmul_rn(__dmul_rn(ns, r), r);
     }
-    const float vf = relaxed_to_float(v, dx & 0x80000000u);
-    o.t = guard ? __uint_as_float(0x7f800000u | (dx & 0x80000000u)) : vf;
+    const float vf = relaxed_to_float(v, sd);
+    o.t = guard ? __uint_as_float(0x7f800000u | sd) : vf;
   }
   if constexpr (SEG) {
     o.seg_sc = static_cast<int>(g);
