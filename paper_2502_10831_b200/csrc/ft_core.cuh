@@ -736,15 +736,15 @@ __device__ __forceinline__ Out3 fast_taylor(double x, int n) {
 // of the reference's own binary64 result rounds to the same float or to a
 // neighbour (<= 1 ulp).  That frees the reduction and the evaluation:
 //
-//   * one signed reduction for all three functions: m = rint(x/pi) from one
-//     FMA with 1.5*2^52 (m in the low word, two's complement), d = RN(x - pi*m)
-//     by one FMA.  |d| is the distance from |x| to the nearest multiple of pi,
-//     which is what reduce_sin / reduce_cos / reduce_tan all compute on |x|
-//     (the quadrant fold of reduction.hpp:44-52 and the tangent's r > pi/2
-//     fold of :88-89 both pick the nearest multiple of pi; m and d of x are
-//     the exact negatives of those of -x), so red = red_t = |d| and the signs
-//     are bits: sin (d<0) ^ (m odd), cos (m odd), tan (d<0) -- the reference's
-//     signbit(x) flips (reduction.hpp:66,91) are already in d.
+//   * one signed reduction for all three functions: m = rint(|x|/pi) from one
+//     FMA with 1.5*2^52 (m in the low word), d = RN(|x| - pi*m) by one FMA.
+//     |d| is the distance from |x| to the nearest multiple of pi, which is
+//     what reduce_sin / reduce_cos / reduce_tan all compute (the quadrant fold
+//     of reduction.hpp:44-52 and the tangent's r > pi/2 fold of :88-89 both
+//     pick the nearest multiple of pi), so red = red_t = |d| and the signs are
+//     bits: sin (d<0) ^ (m odd) ^ (x<0), cos (m odd), tan (d<0) ^ (x<0).  The
+//     tan-only kernels reduce the signed x instead (relaxed_x<true>): m and d
+//     are then the exact negatives, and the tangent's sign is d's alone.
 //     The reference's red differs from |d| only by the rounding of RN(2pi*k)
 //     (resp. RN(pi*k)) -- its other subtractions are exact (Sterbenz) -- so
 //     |red_ref - |d|| <= 2^-38 for |x| < 2^16 (2^-37.9 with d's own rounding);
@@ -823,29 +823,24 @@ struct Out3f {
 
 __device__ __forceinline__ float xor_f(float v, unsigned bits) { return __uint_as_float(__float_as_uint(v) ^ bits); }
 
-// The reduction's argument and the sign word of the folded angle.  FT_RELAX_SIGNED
-// = 1 reduces the signed x: m = rint(x/pi) and d = x - m pi are the exact
-// negatives of the |x| reduction's (RN is odd-symmetric, and x/pi never falls
-// on a rounding tie for |x| < 2^52), so red = |d| is unchanged and the sign of x
-// is already in d: one LOP3 fewer per element.  (F2F on the XU pipe; an integer
-// re-bias measured slower, r02l.)
-#ifndef FT_RELAX_SIGNED
-#define FT_RELAX_SIGNED 1
-#endif
+// The reduction's argument and the sign word of the folded angle.  SIGNED
+// reduces the signed x: m = rint(x/pi) and d = x - m pi are the exact negatives
+// of the |x| reduction's (RN is odd-symmetric, and x/pi never falls on a
+// rounding tie for |x| < 2^52), so red = |d| is unchanged and the sign of x is
+// already in d.  Used by the tan-only kernels (one LOP3 fewer per element);
+// the fused kernels reduce |x| (the abs is a free F2F modifier, and their sine
+// sign then needs one LOP3 fewer; r02bc, r02bk).  (F2F on the XU pipe; an
+// integer re-bias measured slower, r02l.)
+template <bool SIGNED>
 __device__ __forceinline__ double relaxed_x(float xf) {
-#if FT_RELAX_SIGNED
-  return static_cast<double>(xf);
-#else
-  return fabs(static_cast<double>(xf));
-#endif
+  if constexpr (SIGNED) return static_cast<double>(xf);
+  else return fabs(static_cast<double>(xf));
 }
 // Bit 31: (d < 0) ^ (x < 0) of the |x| reduction.
+template <bool SIGNED>
 __device__ __forceinline__ unsigned relaxed_dx(double d, float xf) {
-#if FT_RELAX_SIGNED
-  return static_cast<unsigned>(__double2hiint(d));
-#else
-  return static_cast<unsigned>(__double2hiint(d)) ^ __float_as_uint(xf);
-#endif
+  if constexpr (SIGNED) return static_cast<unsigned>(__double2hiint(d));
+  else return static_cast<unsigned>(__double2hiint(d)) ^ __float_as_uint(xf);
 }
 // v to float with `sign` (bit 31) applied (a truncating funnel-shift
 // conversion measured slower, r02l).
@@ -857,7 +852,7 @@ template <int SQ, unsigned MASK, bool SEG>
 __device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const RelaxTable& tb, int steps, bool* okp) {
   constexpr bool kS = (MASK & kSin) != 0, kC = (MASK & kCos) != 0, kT = (MASK & kTan) != 0;
   const FastConsts& K = c_fast;
-  const double a = relaxed_x(xf);
+  const double a = relaxed_x<MASK == kTan>(xf);
   const double t = __fma_rn(a, K.inv_pi, kRintMagic);
   const double d = __fma_rn(-K.pi, __dadd_rn(t, -kRintMagic), a);
   const double red = fabs(d);
@@ -868,7 +863,7 @@ __device__ __forceinline__ Out3f relaxed_proposed_core(float xf, const RelaxTabl
   bool ok = (fabsf(xf) < kRelaxMaxAbs) & (h > br.x) & (h < br.y);
   if constexpr (kT || SEG) ok = ok & (h != kHiGuard);
   const unsigned modd = static_cast<unsigned>(__double2loint(t)) << 31;  // m odd
-  const unsigned dx = relaxed_dx(d, xf);
+  const unsigned dx = relaxed_dx<MASK == kTan>(d, xf);
   double ca, cb, cc, cd;
   lds_f64x2(ra + offsetof(RelaxRow, a), ca, cb);
   lds_f64x2(ra + offsetof(RelaxRow, c), cc, cd);
@@ -925,7 +920,7 @@ template <int NT, unsigned MASK>
 __device__ __forceinline__ Out3f relaxed_taylor_core(float xf, bool* okp) {
   constexpr bool kS = (MASK & kSin) != 0, kC = (MASK & kCos) != 0, kT = (MASK & kTan) != 0;
   const FastConsts& K = c_fast;
-  const double a = relaxed_x(xf);
+  const double a = relaxed_x<MASK == kTan>(xf);
   const double t = __fma_rn(a, K.inv_pi, kRintMagic);
   const double d = __fma_rn(-K.pi, __dadd_rn(t, -kRintMagic), a);
   const double red = fabs(d);
@@ -934,7 +929,7 @@ __device__ __forceinline__ Out3f relaxed_taylor_core(float xf, bool* okp) {
   if constexpr (kS || kT) ok = ok & (h > kHiRelaxLo);
   ok = ok & (h < (kC ? kHiRelaxCos : kHiHalfPi));
   const unsigned modd = static_cast<unsigned>(__double2loint(t)) << 31;
-  const unsigned dx = relaxed_dx(d, xf);
+  const unsigned dx = relaxed_dx<MASK == kTan>(d, xf);
   const double s2 = __dmul_rn(red, red);
   auto horner = [&](const double* c) {
     double p = c[NT - 1];

@@ -288,6 +288,40 @@ def test_k3_full_cfg2_parity_and_paper_bounds(ft):
     check_against(x, {k: v[idx] for k, v in out.items()}, O.proposed(x, 7, seg=True))
 
 
+def test_full_cfg2_production_kernel_vs_reference_library(ft):
+    """configs[1] at full size through the production kernel (fused, no segment
+    output: TMA bulk stores), every one of the 2^28 x 3 outputs compared bit for
+    bit with the unmodified reference library on the host cores (chunks of 2^25
+    elements) -- no device-side oracle involved."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    w = CONFIGS["cfg2"]
+    xd = ft.gen_inputs(w.n, torch.float64, 0, w.lo, w.hi, w.seed)
+    out = ft.proposed_eval(xd, 7)
+    torch.cuda.synchronize()
+    chunk = 1 << 25
+    for lo in range(0, w.n, chunk):
+        x = host(xd[lo:lo + chunk])
+        ref = O.proposed(x, 7, impl="ref")
+        for f in ("sin", "cos", "tan"):
+            assert same_bits(host(out[f][lo:lo + chunk]), ref[f]), (f, lo)
+
+
+def test_full_cfg4_f64_taylor_vs_cpu_oracle(ft):
+    """configs[3] f64 at full size (2^28, Taylor-5 sin+cos, the TMA-store K2)
+    against the CPU restatement of SPEC.md:224-256, bit for bit."""
+    w = CONFIGS["cfg4_f64"]
+    xd = ft.gen_inputs(w.n, torch.float64, 0, w.lo, w.hi, w.seed)
+    out = ft.taylor_eval(xd, w.n_terms, w.mask)
+    torch.cuda.synchronize()
+    chunk = 1 << 25
+    for lo in range(0, w.n, chunk):
+        x = host(xd[lo:lo + chunk])
+        ref = O.taylor(x, w.n_terms, w.mask)
+        for f in ref:
+            assert same_bits(host(out[f][lo:lo + chunk]), ref[f]), (f, lo)
+
+
 def test_tan_stress_cfg3_full(ft):
     """configs[2]: 2^26 f32 near the poles; device-generated x copied to the host
     oracle; bitwise parity, +-inf count (~68%), finite max error vs libm."""
