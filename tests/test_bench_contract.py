@@ -66,6 +66,8 @@ def test_our_arm_line():
     bu = d["burst"]
     assert bu["value"] > 0 and bu["steps"] >= 3 and 0 < bu["roofline_frac"] < 1.2
     assert all(c["burst"]["value"] > 0 for c in d["configs"].values())
+    ax = d["aux_kernels"]
+    assert ax["k3_parity_reduce"]["gelem_s"] > 0 and ax["k4_gen_inputs"]["gbs_written"] > 0
     su = d["sustained"]
     assert su["value"] > 0 and su["seconds"] >= 1.5 and "sm_mhz" in su["clocks"]
     ev = d["e2e_variants"]

@@ -20,6 +20,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--elements", type=int, default=0)
 ap.add_argument("--mode", default="fisr1")
 ap.add_argument("--mask", type=int, default=0)
+ap.add_argument("--check", action="store_true", help="also launch K3 (parity/error reduction) once")
 a = ap.parse_args()
 w = CONFIGS[a.config]
 n = a.elements or min(w.n, 1 << 30)
@@ -33,5 +34,8 @@ for _ in range(a.reps):
         ft.proposed_eval(x, mask, mode, out=out)
     else:
         ft.taylor_eval(x, w.n_terms, mask, out=out)
+if a.check:
+    st = ft.parity_reduce(x, out, mask, kind=w.kind, mode=mode, n_terms=w.n_terms, ulp_tol=2)
+    print("K3", {k: st[k] for k in ("n_checked", "max_ulp", "n_bit_mismatch")})
 torch.cuda.synchronize()
 print(f"ran {a.reps} x {a.config} n={n} mask={mask} mode={a.mode}")
