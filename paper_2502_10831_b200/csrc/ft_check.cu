@@ -64,10 +64,13 @@ __device__ __forceinline__ double warp_sumd(double v) {
 }
 
 struct Acc {
-  std::uint64_t n = 0;
-  std::uint64_t max_ulp[3] = {0, 0, 0}, over[3] = {0, 0, 0}, seg_mm[2] = {0, 0};
-  std::uint64_t inf[3] = {0, 0, 0}, nan[3] = {0, 0, 0}, nfin[3] = {0, 0, 0}, cks[3] = {0, 0, 0};
-  std::uint64_t bits[3] = {0, 0, 0};  // raw-bit mismatches (ulp_dist treats +0 and -0 as equal)
+  // per-thread counters fit 32 bits (a launch gives a thread < 2^32 elements);
+  // they are widened in the warp fold
+  unsigned n = 0;
+  unsigned over[3] = {0, 0, 0}, seg_mm[2] = {0, 0};
+  unsigned inf[3] = {0, 0, 0}, nan[3] = {0, 0, 0}, nfin[3] = {0, 0, 0};
+  unsigned bits[3] = {0, 0, 0};  // raw-bit mismatches (ulp_dist treats +0 and -0 as equal)
+  std::uint64_t max_ulp[3] = {0, 0, 0}, cks[3] = {0, 0, 0};
   // non-negative doubles kept as bit patterns (ordered like the values)
   std::uint64_t max_or[3] = {0, 0, 0}, max_abs[3] = {0, 0, 0}, max_rel[3] = {0, 0, 0};
   double sum_abs[3] = {0, 0, 0}, sum_rel[3] = {0, 0, 0};
@@ -75,9 +78,34 @@ struct Acc {
 
 __device__ __forceinline__ std::uint64_t umax(std::uint64_t a, std::uint64_t b) { return a > b ? a : b; }
 
+// One element's inputs, loaded one iteration ahead of their use (K3 runs at 2-3
+// blocks/SM: without the prefetch a third of its stall samples were the loads).
 template <typename T>
-__device__ __forceinline__ T load_ref(const CheckArgs& a, int j, std::size_t i, double x) {
-  if (a.ref[j]) return static_cast<const T*>(a.ref[j])[i];
+struct Elem {
+  T x;
+  T got[3];
+  T ref[3];
+};
+
+template <typename T>
+__device__ __forceinline__ Elem<T> load_elem(const CheckArgs& a, std::size_t i) {
+  Elem<T> e;
+  e.x = static_cast<const T*>(a.x)[i];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    e.got[j] = T(0);
+    e.ref[j] = T(0);
+    if (a.mask & (1u << j)) {
+      e.got[j] = static_cast<const T*>(a.got[j])[i];
+      if (a.ref[j]) e.ref[j] = static_cast<const T*>(a.ref[j])[i];
+    }
+  }
+  return e;
+}
+
+template <typename T>
+__device__ __forceinline__ T oracle_value(const CheckArgs& a, int j, const Elem<T>& e, double x) {
+  if (a.ref[j]) return e.ref[j];
   int seg = 0;
   double v;
   if (a.kind == 0) v = mirror_proposed(c_table, j, x, a.method, a.steps, &seg);
@@ -86,35 +114,51 @@ __device__ __forceinline__ T load_ref(const CheckArgs& a, int j, std::size_t i, 
   else return v;
 }
 
+#ifndef FT_MINB_K3
+#define FT_MINB_K3 2
+#endif
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_check(const CheckArgs a) {
+__global__ void __launch_bounds__(kThreads, FT_MINB_K3) k_check(const CheckArgs a) {
   Acc acc;
   const std::size_t tid = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
   const std::size_t stride = static_cast<std::size_t>(gridDim.x) * blockDim.x;
-  const T* __restrict__ x = static_cast<const T*>(a.x);
+  Elem<T> cur{};
+  if (tid < a.n) cur = load_elem<T>(a, tid);
   for (std::size_t i = tid; i < a.n; i += stride) {
-    const double xd = static_cast<double>(x[i]);
+    Elem<T> nxt{};
+    if (i + stride < a.n) nxt = load_elem<T>(a, i + stride);
+    const double xd = static_cast<double>(cur.x);
     acc.n += 1;
+    // CUDA libm in binary64 (the error reference); sincos(x) is bitwise sin(x),
+    // cos(x) (tools/sincos_identity.cu: 0 mismatches in 2^32 arguments) and
+    // shares their argument reduction.
+    double lib[3] = {0.0, 0.0, 0.0};
+    if ((a.mask & 3u) == 3u) sincos(xd, &lib[0], &lib[1]);
+    else if (a.mask & 1u) lib[0] = sin(xd);
+    else if (a.mask & 2u) lib[1] = cos(xd);
+    if (a.mask & 4u) lib[2] = tan(xd);
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       if (!(a.mask & (1u << j))) continue;
-      const T got = static_cast<const T*>(a.got[j])[i];
-      const T want = load_ref<T>(a, j, i, xd);
-      const std::uint64_t u = ulp_dist<T>(got, want);
-      acc.max_ulp[j] = umax(acc.max_ulp[j], u);
-      acc.over[j] += u > a.ulp_tol;
+      const T got = cur.got[j];
+      const T want = oracle_value<T>(a, j, cur, xd);
       const std::uint64_t bg = isnan(got) ? Bits<T>::kNaN : Bits<T>::raw(got);
       const std::uint64_t bw = isnan(want) ? Bits<T>::kNaN : Bits<T>::raw(want);
-      acc.bits[j] += bg != bw;
-      const double g = static_cast<double>(got), w = static_cast<double>(want);
-      if (isfinite(g) && isfinite(w)) acc.max_or[j] = umax(acc.max_or[j], d2u(fabs(g - w)));
+      const double g = static_cast<double>(got);
+      if (bg != bw) {  // identical bits (the usual case): 0 ulp, no mismatch, |g - w| = 0
+        const std::uint64_t u = ulp_dist<T>(got, want);
+        acc.max_ulp[j] = umax(acc.max_ulp[j], u);
+        acc.over[j] += u > a.ulp_tol;
+        acc.bits[j] += 1;
+        const double w = static_cast<double>(want);
+        if (isfinite(g) && isfinite(w)) acc.max_or[j] = umax(acc.max_or[j], d2u(fabs(g - w)));
+      }
       acc.inf[j] += isinf(g);
       acc.nan[j] += isnan(g);
       acc.cks[j] += bg;
-      const double lib = j == 0 ? sin(xd) : j == 1 ? cos(xd) : tan(xd);
-      if (isfinite(g) && isfinite(lib)) {
-        const double e = fabs(g - lib);
-        const double r = fabs(lib) > 1e-12 ? e / fabs(lib) : 0.0;
+      if (isfinite(g) && isfinite(lib[j])) {
+        const double e = fabs(g - lib[j]);
+        const double r = fabs(lib[j]) > 1e-12 ? e / fabs(lib[j]) : 0.0;
         acc.nfin[j] += 1;
         acc.max_abs[j] = umax(acc.max_abs[j], d2u(e));
         acc.max_rel[j] = umax(acc.max_rel[j], d2u(r));
@@ -133,6 +177,7 @@ __global__ void __launch_bounds__(kThreads) k_check(const CheckArgs a) {
         acc.seg_mm[1] += a.seg_t[i] != static_cast<std::uint8_t>(s1);
       }
     }
+    cur = nxt;
   }
   // warp fold, one atomic per statistic per warp
   ft_stats* st = a.stats;
