@@ -103,12 +103,17 @@ __device__ __forceinline__ Elem<T> load_elem(const CheckArgs& a, std::size_t i) 
   return e;
 }
 
-template <typename T>
+// SPEC 1: the common call -- proposed functions in the default SqrtMode
+// (fisr, one Newton step) against the device restatement -- with the mode
+// folded into the code; SPEC 0: everything else (runtime mode, Taylor, host
+// oracle arrays).
+template <typename T, int SPEC>
 __device__ __forceinline__ T oracle_value(const CheckArgs& a, int j, const Elem<T>& e, double x) {
-  if (a.ref[j]) return e.ref[j];
+  if (SPEC == 0 && a.ref[j]) return e.ref[j];
   int seg = 0;
   double v;
-  if (a.kind == 0) v = mirror_proposed(c_table, j, x, a.method, a.steps, &seg);
+  if (SPEC == 1) v = mirror_proposed(c_table, j, x, 1, 1, &seg);
+  else if (a.kind == 0) v = mirror_proposed(c_table, j, x, a.method, a.steps, &seg);
   else v = mirror_taylor(c_taylor, j, x, a.n_terms);
   if constexpr (sizeof(T) == 4) return __double2float_rn(v);
   else return v;
@@ -117,7 +122,7 @@ __device__ __forceinline__ T oracle_value(const CheckArgs& a, int j, const Elem<
 #ifndef FT_MINB_K3
 #define FT_MINB_K3 2
 #endif
-template <typename T>
+template <typename T, int SPEC>
 __global__ void __launch_bounds__(kThreads, FT_MINB_K3) k_check(const CheckArgs a) {
   Acc acc;
   const std::size_t tid = blockIdx.x * static_cast<std::size_t>(blockDim.x) + threadIdx.x;
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, FT_MINB_K3) k_check(const CheckArgs 
     for (int j = 0; j < 3; ++j) {
       if (!(a.mask & (1u << j))) continue;
       const T got = cur.got[j];
-      const T want = oracle_value<T>(a, j, cur, xd);
+      const T want = oracle_value<T, SPEC>(a, j, cur, xd);
       const std::uint64_t bg = isnan(got) ? Bits<T>::kNaN : Bits<T>::raw(got);
       const std::uint64_t bw = isnan(want) ? Bits<T>::kNaN : Bits<T>::raw(want);
       const double g = static_cast<double>(got);
@@ -215,14 +220,21 @@ __global__ void __launch_bounds__(kThreads, FT_MINB_K3) k_check(const CheckArgs 
 #undef FT_SUM
 }
 
-template <typename T>
-cudaError_t check_go(const CheckArgs& a, cudaStream_t s) {
+template <typename T, int SPEC>
+cudaError_t check_launch(const CheckArgs& a, cudaStream_t s) {
   unsigned blocks = 0;
-  if (const cudaError_t eg = persistent_blocks(reinterpret_cast<const void*>(k_check<T>), kThreads, a.n, &blocks))
+  if (const cudaError_t eg =
+          persistent_blocks(reinterpret_cast<const void*>(k_check<T, SPEC>), kThreads, a.n, &blocks))
     return eg;
-  k_check<T><<<blocks, kThreads, 0, s>>>(a);
+  k_check<T, SPEC><<<blocks, kThreads, 0, s>>>(a);
   count_launch();
   return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t check_go(const CheckArgs& a, cudaStream_t s) {
+  const bool spec = a.kind == 0 && a.method == 1 && a.steps == 1 && !a.ref[0] && !a.ref[1] && !a.ref[2];
+  return spec ? check_launch<T, 1>(a, s) : check_launch<T, 0>(a, s);
 }
 
 }  // namespace
