@@ -510,6 +510,32 @@ def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0
         "nan_count": st["n_nan"], "checksum": st["checksum"], "outputs": names,
         "oracle": "device restatement of the reference (ft_mirror_*), bitwise-pinned to the CPU oracle",
     }
+    # configs[3]: "measured side by side with the piecewise kernel" -- the proposed
+    # functions of the same mask on the same x, same steps, same checks
+    side = None
+    if w.kind == 1:
+        out_p = {nm: torch.empty_like(x) for nm in names}
+
+        def step_p(i=0):
+            ft.proposed_eval(x, w.mask, mode, out=out_p)
+
+        with ft.f32_policy(policy):
+            for _ in range(3):
+                step_p()
+            torch.cuda.synchronize()
+            ctx.barrier()
+            ms_p_local = time_steps(step_p, steps, stream)
+            ctx.barrier()
+        ms_p = ctx.max_over_ranks(ms_p_local)
+        st_p = reduce_stats(ft.parity_reduce(x, out_p, w.mask, kind=0, mode=mode, ulp_tol=2), device=ctx.coll_device)
+        side = {"kernel": "k_proposed (K1)" + (" relaxed f32" if w.itemsize == 4 and policy == "ulp2" else ""),
+                "outputs": names, "value": round(total / (ms_p / 1e3) / 1e9, 4), "unit": "Gelem/s",
+                "ms_per_step": round(ms_p, 5), "steps": steps,
+                "roofline_frac": round(w.bytes_per_elem * n / (ms_p_local / 1e3) / 1e9 / peak, 4),
+                "max_ulp_vs_oracle": st_p["max_ulp"], "max_abs_err_vs_libm": st_p["max_abs_vs_libm"],
+                "avg_abs_err_vs_libm": [s_ / max(1, c) for s_, c in zip(st_p["sum_abs_vs_libm"],
+                                                                         st_p["n_finite_libm"])]}
+        del out_p
     if bw:
         bms = bw["ms_per_step"]
         bw = {"value": round(total / (bms / 1e3) / 1e9, 4), "unit": "Gelem/s", "ms_per_step": round(bms, 5),
@@ -521,6 +547,8 @@ def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0
              "config": config_dict(w, n, ctx.world, policy, rot), "roofline": roofline,
              "fp64_roof": fp64_roof(w.name, n / (ms_local / 1e3) / 1e9), "gpu_launches": int(launches),
              "clocks": clk, "burst": bw, "aux_kernels": aux, "accuracy": accuracy}
+    if side:
+        entry["piecewise_side_by_side"] = side
     state = {"x": x, "out": out, "n": n, "total": total, "names": names, "tdt": tdt} if keep else None
     del sets
     if not keep:

@@ -80,6 +80,9 @@ def test_our_arm_line():
         assert 0 < c["roofline"]["frac"] < 1.2
         assert c["accuracy"]["over_2ulp"] == [0, 0, 0] and max(c["accuracy"]["max_ulp_vs_oracle"]) <= 2
         assert c["config"]["f32_policy"] == "ulp2"
+    sb = d["configs"]["cfg4_f32"]["piecewise_side_by_side"]  # configs[3]: Taylor beside the piecewise kernel
+    assert sb["value"] > 0 and sb["outputs"] == ["sin", "cos"] and max(sb["max_ulp_vs_oracle"]) <= 2
+    assert sb["max_abs_err_vs_libm"][0] > 100 * d["configs"]["cfg4_f32"]["accuracy"]["max_abs_err_vs_libm"][0]
     assert "rotate over 3 copies" in d["configs"]["cfg1"]["config"]["l2"]
     assert d["configs"]["cfg1"]["gpu_launches"] == 2000
 
