@@ -234,6 +234,16 @@ int stage_reserve(Staging& g, std::size_t bytes) {
 // (~2000 thread creations per 2^28-element call); the calling thread works on
 // its own job too, and concurrent callers (one per device in host_sharded)
 // share the workers.
+extern "C" void ft_copy_stream(void* dst, const void* src, std::size_t n);  // ft_hostcopy.cpp
+// FT_HOST_NT=0 in the environment keeps the cached memcpy (measurements).
+bool stream_copies() {
+  static const bool on = [] {
+    const char* e = std::getenv("FT_HOST_NT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 struct Copy {
   void* dst;
   const void* src;
@@ -294,7 +304,8 @@ class CopyPool {
   static void work(Job& j) {
     std::size_t i;
     while ((i = j.next.fetch_add(1)) < j.parts.size()) {
-      std::memcpy(j.parts[i].dst, j.parts[i].src, j.parts[i].bytes);
+      if (stream_copies()) ft_copy_stream(j.parts[i].dst, j.parts[i].src, j.parts[i].bytes);
+      else std::memcpy(j.parts[i].dst, j.parts[i].src, j.parts[i].bytes);
       if (j.done.fetch_add(1) + 1 == j.parts.size()) {
         std::lock_guard<std::mutex> lk(j.m);
         j.cv.notify_all();
