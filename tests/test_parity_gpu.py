@@ -392,6 +392,30 @@ def test_host_batch_api(ft):
         assert same_bits(t[f], ref[f])
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_host_staged_path_misaligned_views_and_guard_bands(ft, dtype):
+    """Pageable buffers at odd element offsets (destinations not 64-byte aligned,
+    sizes not multiples of the copy block or the staging chunk) through the staged
+    host path, whose pool copies use non-temporal stores on an aligned middle
+    part: results bitwise equal to the oracle, nothing written outside the views."""
+    n = (5 << 20) + 12345  # three staging chunks, ragged tail
+    w = CONFIGS["cfg2"]
+    base = O.gen_uniform(n + 64, w.lo, w.hi, w.seed).astype(dtype)
+    canary = dtype(-777.25)
+    for xo, oo in ((1, 3), (7, 0), (0, 5)):
+        x = base[xo:xo + n]
+        bufs = {nm: np.full(n + 64, canary, dtype) for nm in ("sin", "cos", "tan")}
+        outs = {nm: b[oo:oo + n] for nm, b in bufs.items()}
+        ft.proposed_batch(x, 7, out=outs)
+        ref = O.proposed(np.ascontiguousarray(x), 7)
+        for nm, b in bufs.items():
+            assert same_bits(outs[nm], ref[nm]), (nm, xo, oo)
+            assert np.all(b[:oo] == canary) and np.all(b[oo + n:] == canary), (nm, xo, oo)
+    # a single-output reference-shaped call on the same kind of view
+    x = base[3:3 + n].astype(np.float64)
+    assert same_bits(ft.proposed_tan_batch(x), O.proposed(x, 4)["tan"])
+
+
 def test_paper_protocol_bounds_from_gpu(ft):
     """PAPER.md:240 protocol through the GPU path; host glibc as the reference."""
     p = PAPER_PROTOCOL
