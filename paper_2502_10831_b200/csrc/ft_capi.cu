@@ -186,7 +186,16 @@ int pipe_reserve(HostPipe& p, std::size_t bytes) {
 // Pageable host memory (e.g. the std::vector the reference API returns) goes
 // through a pinned staging ring: parallel host memcpys into / out of pinned
 // slots, overlapped with the H2D / kernel / D2H streams of other chunks.
-constexpr std::size_t kStageChunk = std::size_t(1) << 21;  // elements per staged chunk
+// Bytes per array per staged chunk (16 MiB: 2 Mi f64 / 4 Mi f32 elements;
+// FT_STAGE_MB overrides it for measurements).
+std::size_t stage_bytes() {
+  static const std::size_t b = [] {
+    const char* e = std::getenv("FT_STAGE_MB");
+    const long mb = e ? std::atol(e) : 16;
+    return static_cast<std::size_t>(mb >= 1 && mb <= 256 ? mb : 16) << 20;
+  }();
+  return b;
+}
 struct Staging {
   void* pin[kPipe][4]{};  // x, sin, cos, tan
   cudaEvent_t done[kPipe]{};
@@ -372,7 +381,7 @@ int host_pipeline(int dtype, const void* x, std::size_t n, unsigned mask, void* 
   if (const int rc = device_or_fail(&dev)) return rc;
   HostPipe& p = g_pipe[dev];
   std::lock_guard<std::mutex> lk(p.mu);
-  int rc = pipe_reserve(p, std::max(chunk, kStageChunk) * es);  // device slots serve both paths
+  int rc = pipe_reserve(p, std::max(chunk * es, stage_bytes()));  // device slots serve both paths
   if (rc) return rc;
   rc = host_pipeline_locked(p, dev, es, chunk, x, n, mask, out, launch);
   if (rc) {
@@ -398,7 +407,8 @@ int host_pipeline_locked(HostPipe& p, int dev, std::size_t es, std::size_t chunk
   if (!x_pinned || !o_pinned) {
     // ---- staged path for pageable buffers ----
     Staging& g = g_stage[dev];
-    if ((rc = stage_reserve(g, kStageChunk * es))) return rc;
+    if ((rc = stage_reserve(g, stage_bytes()))) return rc;
+    const std::size_t kStageChunk = stage_bytes() / es;  // elements per staged chunk
     struct Pending {
       bool live = false;
       std::size_t off = 0, m = 0;
