@@ -509,6 +509,31 @@ def test_host_batch_api_every_sqrt_mode(ft, mode):
         assert same_bits(r[f], ref[f]), f
 
 
+@pytest.mark.parametrize("lo", [0x00000000, 0xFFFFFFFF, 0x80000000, 0x00000001, 0x5A5A5A5A])
+def test_every_f64_high_word_production_kernel(ft, lo):
+    """All 2^32 doubles with the given low word -- every sign, exponent and
+    top-20-bit mantissa, incl. subnormals, infinities and NaNs: every value the
+    fast path's high-word compares (quadrant thresholds, row brackets, guard) can
+    see -- through the production fused f64 kernel (TMA bulk stores), K3 against
+    the device restatement: 0 raw-bit mismatches.  (tools/f64_hiword_sweep.py
+    runs 64 low words in every SqrtMode: profiles/r02cd_f64_hiword.jsonl.)"""
+    chunk = 1 << 28
+    out = None
+    nan = 0
+    for start in range(0, 1 << 32, chunk):
+        hi = torch.arange(start, start + chunk, dtype=torch.int64, device="cuda")
+        x = ((hi << 32) | lo).view(torch.float64)
+        del hi
+        if out is None:
+            out = {nm: torch.empty_like(x) for nm in ("sin", "cos", "tan")}
+        ft.proposed_eval(x, 7, out=out)
+        st = ft.parity_reduce(x, out, 7, ulp_tol=0)
+        assert st["n_checked"] == chunk
+        assert st["n_bit_mismatch"] == [0, 0, 0] and st["max_ulp"] == [0, 0, 0], (hex(start), hex(lo))
+        nan += st["n_nan"][0]
+    assert nan == 2 * (1 << 20)  # exponent 0x7ff, either sign: infinities and NaNs give NaN (reduction.hpp:60-62)
+
+
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 def test_random_bit_patterns_full_range(ft, dtype):
     """2^26 uniformly random bit patterns (every exponent and sign, incl. subnormals,
