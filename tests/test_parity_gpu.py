@@ -248,6 +248,33 @@ def test_mirror_kernel_is_the_oracle(ft):
         assert same_bits(host(out[f]), ref[f])
 
 
+def test_mirror_vs_reference_library_over_the_high_words(ft):
+    """K3's oracle against the unmodified reference over the whole binary64
+    range: every 32nd high word (2^27 doubles: every sign and exponent, 15 top
+    mantissa bits, seeded random low words) evaluated by the device restatement
+    and by oracle/_ref on the host, all three functions and both segment
+    choices bit for bit, in the default SqrtMode and in exact mode."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    n = 1 << 27
+    gen = torch.Generator(device="cuda").manual_seed(77)
+    hi = torch.arange(0, 1 << 32, 32, dtype=torch.int64, device="cuda")
+    lo = torch.randint(0, 1 << 32, (n,), dtype=torch.int64, device="cuda", generator=gen)
+    xd = ((hi << 32) | lo).view(torch.float64)
+    del hi, lo
+    chunk = 1 << 25
+    for m, s in ((1, 1), (0, 0)):
+        out = ft.mirror_eval(xd, 7, 0, ft.SqrtMode(m, s), seg=True)
+        torch.cuda.synchronize()
+        for c0 in range(0, n, chunk):
+            x = host(xd[c0:c0 + chunk])
+            ref = O.proposed(x, 7, m, s, seg=True, impl="ref")
+            for f in ("sin", "cos", "tan"):
+                assert same_bits(host(out[f][c0:c0 + chunk]), ref[f]), (f, m, s, c0)
+            assert np.array_equal(host(out["seg_sc"][c0:c0 + chunk]), ref["seg_sc"])
+            assert np.array_equal(host(out["seg_t"][c0:c0 + chunk]), ref["seg_t"])
+
+
 def test_k3_with_host_oracle_arrays(ft):
     w = CONFIGS["cfg1"]
     x = O.gen_uniform(1 << 20, w.lo, w.hi, w.seed, 0, np.float32)
