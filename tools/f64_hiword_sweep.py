@@ -25,6 +25,8 @@ ap.add_argument("--lo", nargs="+", default=["0"])
 ap.add_argument("--random", type=int, default=0, help="also this many seeded random low words")
 ap.add_argument("--mode", default="fisr1", choices=["fisr1", "exact", "fisr2"])
 ap.add_argument("--chunk", type=int, default=1 << 28)
+ap.add_argument("--taylor", type=int, default=0, help="N > 0: the Taylor kernel K2 with N terms instead of K1")
+ap.add_argument("--mask", type=int, default=7)
 a = ap.parse_args()
 mode = {"fisr1": ft.SqrtMode(), "exact": ft.SqrtMode.exact(), "fisr2": ft.SqrtMode.fisr(2)}[a.mode]
 los = [int(v, 16) for v in a.lo]
@@ -40,9 +42,13 @@ for lo in los:
         x = ((hi << 32) | lo).view(torch.float64)
         del hi
         if out is None:
-            out = {nm: torch.empty_like(x) for nm in ("sin", "cos", "tan")}
-        ft.proposed_eval(x, 7, mode, out=out)
-        st = ft.parity_reduce(x, out, 7, mode=mode, ulp_tol=0)
+            out = {nm: torch.empty_like(x) for j, nm in enumerate(("sin", "cos", "tan")) if a.mask & (1 << j)}
+        if a.taylor:
+            ft.taylor_eval(x, a.taylor, a.mask, out=out)
+            st = ft.parity_reduce(x, out, a.mask, kind=1, n_terms=a.taylor, ulp_tol=0)
+        else:
+            ft.proposed_eval(x, a.mask, mode, out=out)
+            st = ft.parity_reduce(x, out, a.mask, mode=mode, ulp_tol=0)
         tot["n"] += st["n_checked"]
         for j in range(3):
             tot["max_ulp"][j] = max(tot["max_ulp"][j], st["max_ulp"][j])
@@ -50,6 +56,7 @@ for lo in los:
             tot["nan"][j] += st["n_nan"][j]
             tot["inf"][j] += st["n_inf"][j]
         del x
-    print(json.dumps({"low_word": f"{lo:08x}", "mode": a.mode, "checked": tot["n"], "max_ulp_vs_restatement": tot["max_ulp"],
+    print(json.dumps({"low_word": f"{lo:08x}", "kernel": f"taylor-{a.taylor}" if a.taylor else "proposed",
+                      "mask": a.mask, "mode": a.mode, "checked": tot["n"], "max_ulp_vs_restatement": tot["max_ulp"],
                       "bit_mismatches": tot["bit_mismatch"], "nan": tot["nan"], "inf": tot["inf"],
                       "seconds": round(time.time() - t0, 1)}), flush=True)
