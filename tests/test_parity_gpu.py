@@ -273,6 +273,13 @@ def test_mirror_vs_reference_library_over_the_high_words(ft):
                 assert same_bits(host(out[f][c0:c0 + chunk]), ref[f]), (f, m, s, c0)
             assert np.array_equal(host(out["seg_sc"][c0:c0 + chunk]), ref["seg_sc"])
             assert np.array_equal(host(out["seg_t"][c0:c0 + chunk]), ref["seg_t"])
+    # the Taylor restatement against the CPU port, same inputs
+    out = ft.mirror_eval(xd, 7, 1, n_terms=5)
+    torch.cuda.synchronize()
+    for c0 in range(0, n, chunk):
+        ref = O.taylor(host(xd[c0:c0 + chunk]), 5, 7)
+        for f in ref:
+            assert same_bits(host(out[f][c0:c0 + chunk]), ref[f]), ("taylor", f, c0)
 
 
 def test_k3_with_host_oracle_arrays(ft):
