@@ -471,6 +471,19 @@ def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0
         launches = ft.launch_count() - l0
         clk = clocks.stop()
         bw = burst_window(ctx, step, stream, ms_local) if burst else None
+        # cfg5 at N=1: one step (2^33 elements, 8 chained launches) is longer than
+        # the pre-limiter window, so also time the shard each GPU of the 8-GPU
+        # configuration processes (2^30 elements, one launch) in that window
+        bshard = None
+        if burst and w.name == "cfg5" and ctx.world == 1 and n > (1 << 30):
+            ns = 1 << 30
+            xs_, os_ = x[:ns], {nm: o[:ns] for nm, o in out.items()}
+
+            def step_shard(i=0):
+                ft.proposed_eval(xs_, w.mask, mode, out=os_)
+
+            bshard = burst_window(ctx, step_shard, stream, ms_local * ns / n)
+            bshard["elements"] = ns
     ms = ctx.max_over_ranks(ms_local)
     value = total / (ms / 1e3) / 1e9
 
@@ -547,6 +560,13 @@ def measure(ctx: Ctx, w, steps: int, warmup: int, policy: str, elements: int = 0
              "config": config_dict(w, n, ctx.world, policy, rot), "roofline": roofline,
              "fp64_roof": fp64_roof(w.name, n / (ms_local / 1e3) / 1e9), "gpu_launches": int(launches),
              "clocks": clk, "burst": bw, "aux_kernels": aux, "accuracy": accuracy}
+    if bshard:
+        sms = bshard["ms_per_step"]
+        entry["burst_8gpu_shard"] = {
+            "elements": bshard["elements"], "value": round(bshard["elements"] / (sms / 1e3) / 1e9, 4),
+            "unit": "Gelem/s", "ms_per_step": round(sms, 5), "steps": bshard["steps"],
+            "roofline_frac": round(w.bytes_per_elem * bshard["elements"] / (sms / 1e3) / 1e9 / peak, 4),
+            "note": "one GPU's share of the 8-GPU configuration (2^33 / 8), timed alone on this GPU"}
     if side:
         entry["piecewise_side_by_side"] = side
     state = {"x": x, "out": out, "n": n, "total": total, "names": names, "tdt": tdt} if keep else None
